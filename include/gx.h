@@ -1,0 +1,250 @@
+/*
+ * gx.h -- C ABI of the B200-native GPUexplore hot path (libgx.so).
+ *
+ * Plain C types only: pointers, sizes, integer status codes.  One opaque
+ * handle per device-resident object.  Every entry point returns
+ *   GX_OK (0), GX_EINPUT (1, bad argument / config -- the reference raises
+ *   ValueError), GX_ETABLE_FULL (2, mirrors TABLE_FULL / CLI exit 2) or
+ *   GX_EINTERNAL (3, CUDA error or invariant violation -- CLI exit 3),
+ * the CLI exit codes of the reference (pkg/src/ltsmc/cli.py:28-31), and
+ * leaves a message for gx_last_error().
+ *
+ * The reference has no FFI (it is pure Python); the interface each entry
+ * point replaces is cited next to it (paths relative to
+ * /root/reference/pkg/src/ltsmc/).  The Python mirror of that interface
+ * lives in paper_1801_05857_b200/ and binds these symbols with ctypes; see
+ * INTEGRATION.md for the binding a maintainer would add to ltsmc itself.
+ *
+ * Threading: one host thread drives one handle; calls are ordered on the
+ * handle's CUDA stream (0 = legacy default stream).  All device memory is
+ * owned by the library.
+ */
+#ifndef GX_H
+#define GX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GX_OK 0
+#define GX_EINPUT 1
+#define GX_ETABLE_FULL 2
+#define GX_EINTERNAL 3
+
+/* slot status values, hashtable.py:35-38 */
+#define GX_EMPTY 0
+#define GX_CLAIMED 1
+#define GX_OCCUPIED_NEW 2
+#define GX_OCCUPIED_OLD 3
+
+/* find_or_insert result codes, hashtable.py:41-43 */
+#define GX_FOUND 0
+#define GX_INSERTED 1
+#define GX_TABLE_FULL 2
+
+/* layouts, hashtable.py:45-46 */
+#define GX_LAYOUT_PLAIN 0
+#define GX_LAYOUT_HALF 1
+
+/* explore outcomes, explore.py:33-35 */
+#define GX_COMPLETE 0
+#define GX_OUTCOME_TABLE_FULL 1
+#define GX_ITERATION_CAP 2
+
+#define GX_DEADLOCK_KEEP 100 /* explore.py:38 */
+
+typedef struct gx_table gx_table;
+typedef struct gx_net gx_net;
+
+/* ------------------------------------------------------------------ table */
+
+/* TableConfig (hashtable.py:75-86) + vector length.  mark_word/mark_bit
+ * name a bit that no key ever sets (a spare high bit of the packing
+ * scheme, statevec.py:41-66); the table then stores keys with that bit
+ * set and needs no status read on the probe path (single 32/64/128-bit
+ * CAS insert).  mark_word = -1: keys may use every bit, and the table runs
+ * the reference's claim/publish protocol on a status byte per slot
+ * (hashtable.py:252-267). */
+typedef struct gx_table_cfg {
+    int32_t bucket_words;       /* 4, 8, 16, 32 */
+    int32_t num_hash_functions; /* K >= 1 (<= 64 here) */
+    uint64_t capacity_words;    /* num_buckets = capacity_words / bucket_words */
+    int32_t layout;             /* GX_LAYOUT_PLAIN / GX_LAYOUT_HALF (resolved) */
+    int32_t vector_length;      /* 1..16 */
+    uint64_t seed;              /* hash seed, hashtable.py:50 */
+    int32_t mark_word;          /* -1: none */
+    int32_t mark_bit;           /* 0..31 */
+} gx_table_cfg;
+
+/* StateTable.__init__ (hashtable.py:137-201).  Allocates and zeroes device
+ * memory.  stream: a cudaStream_t or NULL. */
+int gx_table_create(const gx_table_cfg *cfg, void *stream, gx_table **out);
+int gx_table_destroy(gx_table *t);
+/* Reset to empty (fresh table, same geometry). */
+int gx_table_clear(gx_table *t);
+
+/* num_buckets, slots_per_bucket, total_slots (hashtable.py:155-159) */
+int gx_table_geometry(const gx_table *t, uint64_t *num_buckets, int32_t *slots_per_bucket,
+                      uint64_t *total_slots);
+/* (a_i, b_i) pairs and the fold salt (hashtable.py:199-201), for tests */
+int gx_table_hash_constants(const gx_table *t, uint64_t *a, uint64_t *b, uint64_t *salt);
+
+/* find_or_insert over a batch (hashtable.py:224-280).  keys: n * vlen
+ * words (host memory), codes[n] / handles[n] out (host memory).  Equal
+ * keys in one batch agree on one handle and exactly one gets INSERTED.
+ * serial != 0 processes the batch one key at a time in order on one warp:
+ * the reference's single-threaded placement, handle for handle. */
+int gx_find_or_put(gx_table *t, const uint32_t *keys, uint64_t n, uint8_t *codes,
+                   int64_t *handles, int32_t serial);
+/* Same on device-resident buffers (keys/codes/handles are device
+ * pointers; codes/handles may be NULL).  *inserted (host) gets the number
+ * of INSERTED results, *full the number of TABLE_FULL results. */
+int gx_find_or_put_device(gx_table *t, const uint32_t *d_keys, uint64_t n, uint8_t *d_codes,
+                          int64_t *d_handles, uint64_t *inserted, uint64_t *full);
+
+/* claim_new (hashtable.py:296-313): claimed[i] = 1 iff this call moved
+ * handles[i] NEW -> OLD.  Repeated handles in one batch: exactly one wins. */
+int gx_claim_new(gx_table *t, const int64_t *handles, uint64_t n, uint8_t *claimed);
+
+/* scan_new (hashtable.py:315-324): handles of NEW slots in buckets
+ * [first, last), ascending (bucket-major).  Call with out = NULL to get the
+ * count in *count; then with capacity >= count. */
+int gx_scan_new(gx_table *t, uint64_t first, uint64_t last, int64_t *out, uint64_t capacity,
+                uint64_t *count);
+
+/* occupancy (hashtable.py:326-331): occupied and new counts. */
+int gx_occupancy(gx_table *t, uint64_t *occupied, uint64_t *new_count);
+
+/* slot_status / read_slot over a batch of handles (hashtable.py:335-342). */
+int gx_read_slots(gx_table *t, const int64_t *handles, uint64_t n, uint8_t *status,
+                  uint32_t *words);
+
+/* occupied_vectors / dump_rows (hashtable.py:344-365): all slots with
+ * status >= NEW in bucket-major order.  out arrays sized by a first call
+ * with NULLs (count in *count). */
+int gx_dump(gx_table *t, int64_t *handles, uint8_t *status, uint32_t *words, uint64_t capacity,
+            uint64_t *count);
+
+/* --------------------------------------------------------------- network */
+
+/* A Network (network.py:43-62) flattened to device CSR by the host
+ * (paper_1801_05857_b200/network.py: to_csr).  All arrays are u32; the
+ * layout of each is documented in DESIGN.md ("network CSR"). */
+typedef struct gx_network_csr {
+    uint32_t nproc, nrules, vlen, reserved;
+    const uint32_t *proc;  uint64_t n_proc;   /* nproc x {word, shift, mask, qbase}       */
+    const uint32_t *qtab;  uint64_t n_qtab;   /* per (proc, state) {off, ndst, count, trig} */
+    const uint32_t *im_dst; uint64_t n_im_dst;/* independent-move destinations            */
+    const uint32_t *trig;  uint64_t n_trig;   /* [n, rule ids...] lists                    */
+    const uint32_t *rules; uint64_t n_rules;  /* nrules x {npart, part_off, dedup_off, res} */
+    const uint32_t *parts; uint64_t n_parts;  /* participants {rq_base, word, shift, mask} */
+    const uint32_t *rq;    uint64_t n_rq;     /* per (rule, part, state) {off, n}          */
+    const uint32_t *rdst;  uint64_t n_rdst;   /* rule destinations                         */
+    const uint32_t *dedup; uint64_t n_dedup;  /* [n, earlier rule ids...] lists            */
+    const uint32_t *initial;                  /* packed initial state, vlen words         */
+} gx_network_csr;
+
+/* build_network (network.py:65-181) result, uploaded once. */
+int gx_net_create(const gx_network_csr *csr, void *stream, gx_net **out);
+int gx_net_destroy(gx_net *n);
+
+/* expand (network.py:184-238) over a batch of packed states (host memory):
+ * counts[i] = transition count, nsucc[i] = successors emitted (self-loops
+ * of independent moves are not emitted; rule targets deduplicated by
+ * (result, target)); succ gets the packed successors back to back when
+ * non-NULL (capacity in vectors).  Test / debug entry point. */
+int gx_expand(gx_net *n, const uint32_t *states, uint64_t nstates, uint64_t *counts,
+              uint32_t *nsucc, uint32_t *succ, uint64_t capacity, uint64_t *total);
+
+/* ---------------------------------------------------------------- explore */
+
+/* ExploreConfig (explore.py:47-62) minus the CPU worker knobs. */
+typedef struct gx_explore_cfg {
+    int32_t detect_deadlocks;
+    int32_t reserved0;
+    int64_t max_iterations;     /* <= 0: none */
+    uint64_t frontier_capacity; /* vectors; 0 = size from free device memory */
+    int32_t probe_group;        /* 0 = auto; else lanes per bucket probe (1,2,4,8) */
+    int32_t reserved1;
+} gx_explore_cfg;
+
+/* ExplorationReport (explore.py:65-88) */
+typedef struct gx_report {
+    uint64_t states, transitions, expanded, iterations, deadlocks_total;
+    int32_t outcome;            /* GX_COMPLETE / GX_OUTCOME_TABLE_FULL / GX_ITERATION_CAP */
+    int32_t deadlocks_kept;     /* <= GX_DEADLOCK_KEEP */
+    double device_ms;           /* CUDA-event time of the level loop */
+    uint64_t levels_launched;   /* expand kernels launched */
+    uint64_t max_frontier;      /* widest BFS level */
+    uint64_t kernels;           /* all kernels launched by this call */
+} gx_report;
+
+/* explore (explore.py:300-395): level-synchronous BFS from the network's
+ * initial state into table t (cleared first).  deadlocks: GX_DEADLOCK_KEEP
+ * * vlen words (host), the smallest deadlock states in packed form
+ * (composite-order sorting is done by the caller).  Table statuses are
+ * left as the reference leaves them: expanded states OLD, states of the
+ * last unexpanded level NEW. */
+int gx_explore(gx_net *n, gx_table *t, const gx_explore_cfg *cfg, gx_report *report,
+               uint32_t *deadlocks);
+
+/* ------------------------------------------------- per-level primitives */
+/* For the hash-owner sharded multi-GPU driver (paper_1801_05857_b200/
+ * distributed.py): expand one level's frontier (device buffer of n packed
+ * states) and bin every successor by owner rank = owner_of(fold) across
+ * `ranks` peers into d_out (device, capacity vectors); d_counts[ranks]
+ * (device u64) gets per-owner counts, successors of owner r occupy
+ * [d_offsets[r], d_offsets[r] + d_counts[r]) after the call (d_offsets
+ * device u64[ranks]).  *transitions / *deadlocks (host) get the level's
+ * totals; deadlock states append to the handle's deadlock buffer. */
+int gx_expand_route(gx_net *n, const gx_table *t, const uint32_t *d_frontier, uint64_t nfront,
+                    int32_t ranks, uint32_t *d_out, uint64_t capacity, uint64_t *d_counts,
+                    uint64_t *d_offsets, uint64_t *transitions, uint64_t *deadlocks,
+                    int32_t detect_deadlocks);
+/* FINDORPUT of n received vectors; INSERTED ones are appended to
+ * d_next (device, capacity vectors); *n_next (host) = appended count. */
+int gx_insert_append(gx_table *t, const uint32_t *d_keys, uint64_t n, uint32_t *d_next,
+                     uint64_t capacity, uint64_t *n_next, int32_t *table_full);
+/* owner_of for a batch of host vectors (tests of the routing function) */
+int gx_owner_of(const gx_table *t, const uint32_t *keys, uint64_t n, int32_t ranks,
+                int32_t *owner);
+
+/* ------------------------------------------------------------ benchmark */
+/* Isolated FINDORPUT benchmark (bench.py:120-202 protocol on device
+ * generated keys): `total` operations, each unique vector repeated
+ * `duplication` times, globally shuffled by a keyed bijection.  Keys are
+ * random words masked to key_bits bits per word (32 = full words).
+ * ms = CUDA-event time of the insert kernel(s) only; found/inserted
+ * counted on device. */
+int gx_bench_find_or_put(gx_table *t, uint64_t total, uint64_t duplication, uint64_t seed,
+                         int32_t key_bits, int32_t probe_group, double *ms, uint64_t *found,
+                         uint64_t *inserted, uint64_t *full);
+
+/* Same, with the unique rows numbered from row_base (so successive calls
+ * can fill a table step by step with fresh keys: the fill-factor sweep). */
+int gx_bench_find_or_put_rows(gx_table *t, uint64_t total, uint64_t duplication, uint64_t row_base,
+                              uint64_t seed, int32_t key_bits, int32_t probe_group, double *ms,
+                              uint64_t *found, uint64_t *inserted, uint64_t *full);
+
+/* ----------------------------------------------------------------- misc */
+/* Insertion protocol chosen at create time: 0 = mark bit (single CAS),
+ * 1 = status-byte claim/publish. */
+int gx_table_mode(const gx_table *t);
+/* Deadlock states recorded by the last gx_expand_route call (device
+ * buffer, at most 65536 kept); *count gets the number recorded. */
+int gx_net_deadlocks(gx_net *n, uint32_t *out, uint64_t capacity, uint64_t *count);
+const char *gx_last_error(void);
+/* Number of kernels this library has launched (process-wide counter). */
+uint64_t gx_kernel_launches(void);
+/* Device properties used for grid sizing. */
+int gx_device_info(int32_t *sm_count, uint64_t *free_bytes, uint64_t *total_bytes);
+/* Synchronise the handle's stream and report asynchronous errors. */
+int gx_sync(void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GX_H */

@@ -1,0 +1,143 @@
+// gx_expand.cuh -- successor generation on packed state vectors
+// (network.py:184-238 semantics, restated on the device CSR).
+#pragma once
+#include "gx_internal.h"
+
+namespace gx {
+
+__device__ __forceinline__ uint32_t field_get(const uint32_t* s, uint32_t word, uint32_t shift,
+                                              uint32_t mask) {
+    return (s[word] >> shift) & mask;
+}
+
+// Does rule r' produce target t from source s?  True iff t differs from s
+// only in r's participants and each participant's value in t is one of its
+// rule destinations at its value in s (network.py:213-237).
+template <int V>
+__device__ __forceinline__ bool rule_generates(const NetDesc& N, uint32_t r, const uint32_t* s,
+                                               const uint32_t* t) {
+    const uint4 rl = __ldg(&N.rules[r]);
+    uint32_t allowed[V];
+#pragma unroll
+    for (int w = 0; w < V; w++) allowed[w] = 0;
+    for (uint32_t k = 0; k < rl.x; k++) {
+        const uint4 pt = __ldg(&N.parts[rl.y + k]);
+#pragma unroll
+        for (int w = 0; w < V; w++)
+            if ((uint32_t)w == pt.y) allowed[w] |= pt.w << pt.z;
+    }
+#pragma unroll
+    for (int w = 0; w < V; w++)
+        if ((s[w] ^ t[w]) & ~allowed[w]) return false;
+    for (uint32_t k = 0; k < rl.x; k++) {
+        const uint4 pt = __ldg(&N.parts[rl.y + k]);
+        const uint32_t sq = field_get(s, pt.y, pt.z, pt.w);
+        const uint32_t tq = field_get(t, pt.y, pt.z, pt.w);
+        const uint2 l = __ldg(&N.rq[pt.x + sq]);
+        bool in = false;
+        for (uint32_t d = 0; d < l.y && !in; d++) in = __ldg(&N.rdst[l.x + d]) == tq;
+        if (!in) return false;
+    }
+    return true;
+}
+
+// Build the target of combination `c` of rule `rl` from s into t.
+template <int V>
+__device__ __forceinline__ void rule_target(const NetDesc& N, const uint4 rl, uint64_t c,
+                                            const uint32_t* s, uint32_t* t) {
+#pragma unroll
+    for (int w = 0; w < V; w++) t[w] = s[w];
+    // mixed radix, last participant fastest (itertools.product order)
+    for (int k = (int)rl.x - 1; k >= 0; k--) {
+        const uint4 pt = __ldg(&N.parts[rl.y + k]);
+        const uint32_t sq = field_get(s, pt.y, pt.z, pt.w);
+        const uint2 l = __ldg(&N.rq[pt.x + sq]);
+        const uint32_t dig = (uint32_t)(c % l.y);
+        c /= l.y;
+        const uint32_t dst = __ldg(&N.rdst[l.x + dig]);
+#pragma unroll
+        for (int w = 0; w < V; w++)
+            if ((uint32_t)w == pt.y) t[w] = (t[w] & ~(pt.w << pt.z)) | (dst << pt.z);
+    }
+}
+
+// Expand packed state s.  Returns the number of successor slots n (the
+// index space of emitted successors) and the transition count in *count.
+// EMIT: successors with index in [lo, hi) are written to out[(idx-lo)*V].
+// Independent self-loops are counted but never emitted (t == s is already
+// in the table); a rule combination whose (result, target) an earlier rule
+// of the same result already produced is neither counted nor emitted
+// (network.py:226-230).
+template <int V, bool EMIT>
+__device__ __forceinline__ uint32_t expand_state(const NetDesc& N, const uint32_t* s,
+                                                 uint64_t* count_out, uint32_t lo, uint32_t hi,
+                                                 uint32_t* out) {
+    uint64_t count = 0;
+    uint32_t n = 0;
+    uint32_t t[V];
+    for (uint32_t i = 0; i < N.nproc; i++) {
+        const uint4 pr = __ldg(&N.proc[i]);
+        const uint32_t q = field_get(s, pr.x, pr.y, pr.z);
+        const uint4 e = __ldg(&N.qtab[pr.w + q]);
+        count += e.z;
+        if (EMIT && n < hi && n + e.y > lo) {
+            for (uint32_t d = 0; d < e.y; d++) {
+                const uint32_t idx = n + d;
+                if (idx < lo || idx >= hi) continue;
+                const uint32_t dst = __ldg(&N.im_dst[e.x + d]);
+                uint32_t* o = out + (uint64_t)(idx - lo) * V;
+#pragma unroll
+                for (int w = 0; w < V; w++)
+                    o[w] = (uint32_t)w == pr.x ? (s[w] & ~(pr.z << pr.y)) | (dst << pr.y) : s[w];
+            }
+        }
+        n += e.y;
+        const uint32_t nt = __ldg(&N.trig[e.w]);
+        for (uint32_t x = 0; x < nt; x++) {
+            const uint32_t r = __ldg(&N.trig[e.w + 1 + x]);
+            const uint4 rl = __ldg(&N.rules[r]);
+            uint64_t combos = 1;
+            for (uint32_t k = 0; k < rl.x; k++) {
+                const uint4 pt = __ldg(&N.parts[rl.y + k]);
+                const uint2 l = __ldg(&N.rq[pt.x + field_get(s, pt.y, pt.z, pt.w)]);
+                combos *= l.y;
+                if (!combos) break;
+            }
+            if (!combos) continue;
+            const uint32_t nd = __ldg(&N.dedup[rl.z]);
+            if (nd == 0) {
+                count += combos;
+                if (EMIT && n < hi && n + combos > lo) {
+                    for (uint64_t c = 0; c < combos; c++) {
+                        const uint64_t idx = n + c;
+                        if (idx < lo || idx >= hi) continue;
+                        rule_target<V>(N, rl, c, s, t);
+                        uint32_t* o = out + (uint64_t)(idx - lo) * V;
+#pragma unroll
+                        for (int w = 0; w < V; w++) o[w] = t[w];
+                    }
+                }
+                n += (uint32_t)combos;
+            } else {
+                for (uint64_t c = 0; c < combos; c++) {
+                    rule_target<V>(N, rl, c, s, t);
+                    bool dup = false;
+                    for (uint32_t y = 0; y < nd && !dup; y++)
+                        dup = rule_generates<V>(N, __ldg(&N.dedup[rl.z + 1 + y]), s, t);
+                    if (dup) continue;
+                    count += 1;
+                    if (EMIT && n >= lo && n < hi) {
+                        uint32_t* o = out + (uint64_t)(n - lo) * V;
+#pragma unroll
+                        for (int w = 0; w < V; w++) o[w] = t[w];
+                    }
+                    n++;
+                }
+            }
+        }
+    }
+    *count_out = count;
+    return n;
+}
+
+}  // namespace gx

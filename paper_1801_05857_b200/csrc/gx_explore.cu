@@ -1,0 +1,1115 @@
+// gx_explore.cu -- level-synchronous BFS on the B200 (reference:
+// explore.py:147-395, network.py:184-238), the per-level primitives of the
+// hash-owner sharded multi-GPU driver, and the isolated FINDORPUT
+// benchmark (bench.py:120-202 protocol).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "gx_expand.cuh"
+#include "gx_internal.h"
+
+namespace gx {
+
+// level counters live in the table's counter block
+enum { LV_NEW = 8, LV_TRANS = 9, LV_EXP = 10, LV_DL = 11, LV_FULL = 12, LV_OVF = 13 };
+
+struct LevelArgs {
+    const uint32_t* front;
+    uint64_t nfront;
+    uint32_t* out;        // next frontier region base
+    uint64_t out_cap;     // vectors in the two-ended frontier buffer
+    uint64_t out_limit;   // max vectors F' may take (cap - |F|)
+    int32_t out_rev;      // F' position p lives at out[rev ? cap-1-p : p]
+    int32_t detect;
+    unsigned long long* ctr;
+    unsigned long long new_base, dl_base;
+    uint32_t* dl;
+    uint64_t dl_cap;
+};
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+    return v;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <int V>
+__device__ __forceinline__ void load_state(const uint32_t* p, uint32_t* s) {
+    if (V == 1) {
+        s[0] = __ldcs(p);
+    } else if (V == 2) {
+        uint2 x = __ldcs(reinterpret_cast<const uint2*>(p));
+        s[0] = x.x;
+        s[1] = x.y;
+    } else if (V == 4) {
+        uint4 x = __ldcs(reinterpret_cast<const uint4*>(p));
+        s[0] = x.x;
+        s[1] = x.y;
+        s[2] = x.z;
+        s[3] = x.w;
+    } else {
+#pragma unroll
+        for (int w = 0; w < V; w++) s[w] = __ldcs(p + w);
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void store_state(uint32_t* p, const uint32_t* s) {
+    if (V == 2) {
+        *reinterpret_cast<uint2*>(p) = make_uint2(s[0], s[1]);
+    } else if (V == 4) {
+        *reinterpret_cast<uint4*>(p) = make_uint4(s[0], s[1], s[2], s[3]);
+    } else {
+#pragma unroll
+        for (int w = 0; w < V; w++) p[w] = s[w];
+    }
+}
+
+// words of shared memory per warp for the successor queue
+constexpr int QWORDS = 1024;
+
+// One BFS level: every warp takes 32 frontier states at a time, counts
+// their successors (count pass), scans the counts, then emits successors
+// into its shared-memory queue in chunks of QWORDS/V and runs FINDORPUT on
+// the queue with G lanes per key.  INSERTED keys are appended to the next
+// frontier with one atomic per warp round.
+template <int BW, int V, int G, bool MARK>
+__global__ void __launch_bounds__(256) k_level(TableDesc T, NetDesc N, LevelArgs A) {
+    constexpr int QCAP = QWORDS / V;
+    __shared__ __align__(16) uint32_t qbuf[8][QWORDS];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    uint32_t* q = qbuf[wid];
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    unsigned long long trans = 0, expanded = 0;
+    for (uint64_t base = warp * 32; base < A.nfront; base += nwarps * 32) {
+        int stop = 0;
+        if (lane == 0)
+            stop = (*(volatile unsigned long long*)&A.ctr[LV_FULL] != 0ull) ||
+                   (*(volatile unsigned long long*)&A.ctr[LV_OVF] != 0ull);
+        if (__shfl_sync(FULLMASK, stop, 0)) break;
+        const uint64_t idx = base + lane;
+        const bool has = idx < A.nfront;
+        uint32_t s[V];
+        if (has)
+            load_state<V>(A.front + idx * V, s);
+        else
+#pragma unroll
+            for (int w = 0; w < V; w++) s[w] = 0;
+        uint64_t cnt = 0;
+        uint32_t n = 0;
+        if (has) {
+            n = expand_state<V, false>(N, s, &cnt, 0, 0, nullptr);
+            trans += cnt;
+            expanded += 1;
+            if (cnt == 0 && A.detect) {
+                unsigned long long p = atomicAdd(&A.ctr[LV_DL], 1ull) - A.dl_base;
+                if (p < A.dl_cap) store_state<V>(A.dl + p * V, s);
+            }
+        }
+        uint32_t incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(FULLMASK, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(FULLMASK, incl, 31);
+        const uint32_t excl = incl - n;
+        for (uint32_t c0 = 0; c0 < total; c0 += QCAP) {
+            const uint32_t c1 = min(total, c0 + (uint32_t)QCAP);
+            if (has && n && excl < c1 && excl + n > c0) {
+                const uint32_t lo = max(c0, excl) - excl;
+                const uint32_t hi = min(c1, excl + n) - excl;
+                uint64_t dummy;
+                expand_state<V, true>(N, s, &dummy, lo, hi, q + (uint64_t)(excl + lo - c0) * V);
+            }
+            __syncwarp();
+            const uint32_t m = c1 - c0;
+            constexpr int R = MARK ? 32 / G : 32;
+            const int grp = MARK ? lane / G : lane;
+            for (uint32_t r0 = 0; r0 < m; r0 += R) {
+                const uint32_t e = r0 + grp;
+                const bool active = e < m;
+                uint32_t key[V];
+#pragma unroll
+                for (int w = 0; w < V; w++) key[w] = active ? q[e * V + w] : 0u;
+                const uint64_t h = fold<V>(T.salt, key);
+                int64_t hd;
+                int code;
+                bool leader;
+                if constexpr (MARK) {
+                    code = probe_mark<BW, V, G>(T, active, key, h, &hd);
+                    leader = active && (lane & (G - 1)) == 0;
+                } else {
+                    code = active ? probe_status(T, key, h, &hd) : FOUND;
+                    leader = active;
+                }
+                const bool ins = leader && code == INSERTED;
+                const bool full = leader && code == TABLE_FULL;
+                if (__any_sync(FULLMASK, full) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
+                const uint32_t insm = __ballot_sync(FULLMASK, ins);
+                if (insm) {
+                    unsigned long long pos0 = 0;
+                    if (lane == 0) pos0 = atomicAdd(&A.ctr[LV_NEW], (unsigned long long)__popc(insm)) - A.new_base;
+                    pos0 = __shfl_sync(FULLMASK, pos0, 0);
+                    if (ins) {
+                        const unsigned long long p = pos0 + __popc(insm & lanemask_lt());
+                        if (p < A.out_limit) {
+                            const uint64_t slot = A.out_rev ? A.out_cap - 1 - p : p;
+                            store_state<V>(A.out + slot * V, key);
+                        } else {
+                            atomicExch(&A.ctr[LV_OVF], 1ull);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    trans = warp_sum(trans);
+    expanded = warp_sum(expanded);
+    if (lane == 0) {
+        if (trans) atomicAdd(&A.ctr[LV_TRANS], trans);
+        if (expanded) atomicAdd(&A.ctr[LV_EXP], expanded);
+    }
+}
+
+typedef void (*level_kernel_t)(TableDesc, NetDesc, LevelArgs);
+
+template <int BW, int V>
+static level_kernel_t pick_level_g(int g) {
+    switch (g) {
+        case 1: return k_level<BW, V, 1, true>;
+        case 2: if (BW >= 8) return k_level<BW, V, (BW >= 8 ? 2 : 1), true>; break;
+        case 4: if (BW >= 16) return k_level<BW, V, (BW >= 16 ? 4 : 1), true>; break;
+        case 8: if (BW >= 32) return k_level<BW, V, (BW >= 32 ? 8 : 1), true>; break;
+    }
+    return nullptr;
+}
+
+template <int BW>
+static level_kernel_t pick_level_v(int v, int g) {
+    switch (v) {
+        case 1: return pick_level_g<BW, 1>(g);
+        case 2: return pick_level_g<BW, 2>(g);
+        case 4: return pick_level_g<BW, 4>(g);
+    }
+    return nullptr;
+}
+
+static level_kernel_t pick_level_status(int v) {
+    switch (v) {
+#define GX_CASE(X) \
+    case X: return k_level<0, X, 1, false>;
+        GX_CASE(1) GX_CASE(2) GX_CASE(3) GX_CASE(4) GX_CASE(5) GX_CASE(6) GX_CASE(7) GX_CASE(8)
+        GX_CASE(9) GX_CASE(10) GX_CASE(11) GX_CASE(12) GX_CASE(13) GX_CASE(14) GX_CASE(15)
+        GX_CASE(16)
+#undef GX_CASE
+    }
+    return nullptr;
+}
+
+int default_group(int bw);
+
+static level_kernel_t pick_level(const TableDesc& T, int group) {
+    if (T.mode == MODE_STATUS) return pick_level_status((int)T.vlen);
+    const int g = group > 0 ? group : default_group((int)T.bw);
+    switch (T.bw) {
+        case 4: return pick_level_v<4>((int)T.vlen, g);
+        case 8: return pick_level_v<8>((int)T.vlen, g);
+        case 16: return pick_level_v<16>((int)T.vlen, g);
+        case 32: return pick_level_v<32>((int)T.vlen, g);
+    }
+    return nullptr;
+}
+
+// ------------------------------------------------------------ gx_expand
+
+template <int V>
+__global__ void k_expand_count(NetDesc N, const uint32_t* __restrict__ states, uint64_t n,
+                               unsigned long long* counts, uint32_t* nsucc) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t s[V];
+#pragma unroll
+    for (int w = 0; w < V; w++) s[w] = states[i * V + w];
+    uint64_t c;
+    nsucc[i] = expand_state<V, false>(N, s, &c, 0, 0, nullptr);
+    counts[i] = c;
+}
+
+template <int V>
+__global__ void k_expand_emit(NetDesc N, const uint32_t* __restrict__ states, uint64_t n,
+                              const unsigned long long* offs, uint32_t* out, uint64_t cap) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t s[V];
+#pragma unroll
+    for (int w = 0; w < V; w++) s[w] = states[i * V + w];
+    const unsigned long long o = offs[i];
+    if (o >= cap) return;
+    uint64_t c;
+    expand_state<V, true>(N, s, &c, 0, (uint32_t)min((unsigned long long)UINT32_MAX, cap - o),
+                          out + o * V);
+}
+
+typedef void (*count_kernel_t)(NetDesc, const uint32_t*, uint64_t, unsigned long long*, uint32_t*);
+typedef void (*emit_kernel_t)(NetDesc, const uint32_t*, uint64_t, const unsigned long long*,
+                              uint32_t*, uint64_t);
+
+static count_kernel_t pick_count(int v) {
+    switch (v) {
+#define GX_CASE(X) \
+    case X: return k_expand_count<X>;
+        GX_CASE(1) GX_CASE(2) GX_CASE(3) GX_CASE(4) GX_CASE(5) GX_CASE(6) GX_CASE(7) GX_CASE(8)
+        GX_CASE(9) GX_CASE(10) GX_CASE(11) GX_CASE(12) GX_CASE(13) GX_CASE(14) GX_CASE(15)
+        GX_CASE(16)
+#undef GX_CASE
+    }
+    return nullptr;
+}
+
+static emit_kernel_t pick_emit(int v) {
+    switch (v) {
+#define GX_CASE(X) \
+    case X: return k_expand_emit<X>;
+        GX_CASE(1) GX_CASE(2) GX_CASE(3) GX_CASE(4) GX_CASE(5) GX_CASE(6) GX_CASE(7) GX_CASE(8)
+        GX_CASE(9) GX_CASE(10) GX_CASE(11) GX_CASE(12) GX_CASE(13) GX_CASE(14) GX_CASE(15)
+        GX_CASE(16)
+#undef GX_CASE
+    }
+    return nullptr;
+}
+
+// ------------------------------------------------- multi-GPU primitives
+
+// owner-binning helpers over a flat successor buffer
+__global__ void k_owner_hist(uint64_t salt, const uint32_t* __restrict__ keys, uint64_t n, int v,
+                             int ranks, unsigned long long* counts) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int o = owner_of(fold_rt(salt, keys + i * v, v), ranks);
+    atomicAdd(&counts[o], 1ull);
+}
+
+__global__ void k_owner_scatter(uint64_t salt, const uint32_t* __restrict__ keys, uint64_t n, int v,
+                                int ranks, unsigned long long* cursor, uint32_t* out) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t* k = keys + i * v;
+    const int o = owner_of(fold_rt(salt, k, v), ranks);
+    const unsigned long long p = atomicAdd(&cursor[o], 1ull);
+    for (int w = 0; w < v; w++) out[p * v + w] = k[w];
+}
+
+__global__ void k_owner_of(uint64_t salt, const uint32_t* __restrict__ keys, uint64_t n, int v,
+                           int ranks, int32_t* out) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = owner_of(fold_rt(salt, keys + i * v, v), ranks);
+}
+
+// expand a frontier into a flat successor buffer (warp-aggregated append)
+template <int V>
+__global__ void __launch_bounds__(256) k_expand_flat(NetDesc N, const uint32_t* __restrict__ front,
+                                                     uint64_t nfront, uint32_t* out, uint64_t cap,
+                                                     unsigned long long* ctr, uint32_t* dl,
+                                                     uint64_t dl_cap, int detect) {
+    // ctr: [0] successors, [1] transitions, [2] deadlocks, [3] overflow
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    unsigned long long trans = 0;
+    for (uint64_t base = warp * 32; base < nfront; base += nwarps * 32) {
+        const uint64_t idx = base + lane;
+        const bool has = idx < nfront;
+        uint32_t s[V];
+        if (has)
+            load_state<V>(front + idx * V, s);
+        else
+#pragma unroll
+            for (int w = 0; w < V; w++) s[w] = 0;
+        uint64_t cnt = 0;
+        uint32_t n = 0;
+        if (has) {
+            n = expand_state<V, false>(N, s, &cnt, 0, 0, nullptr);
+            trans += cnt;
+            if (cnt == 0 && detect) {
+                unsigned long long p = atomicAdd(&ctr[2], 1ull);
+                if (p < dl_cap) store_state<V>(dl + p * V, s);
+            }
+        }
+        uint32_t incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(FULLMASK, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(FULLMASK, incl, 31);
+        unsigned long long b0 = 0;
+        if (lane == 0 && total) b0 = atomicAdd(&ctr[0], (unsigned long long)total);
+        b0 = __shfl_sync(FULLMASK, b0, 0);
+        const unsigned long long my = b0 + incl - n;
+        if (has && n) {
+            if (my + n <= cap) {
+                uint64_t dummy;
+                expand_state<V, true>(N, s, &dummy, 0, n, out + my * V);
+            } else {
+                atomicExch(&ctr[3], 1ull);
+            }
+        }
+    }
+    trans = warp_sum(trans);
+    if (lane == 0 && trans) atomicAdd(&ctr[1], trans);
+}
+
+typedef void (*flat_kernel_t)(NetDesc, const uint32_t*, uint64_t, uint32_t*, uint64_t,
+                              unsigned long long*, uint32_t*, uint64_t, int);
+
+static flat_kernel_t pick_flat(int v) {
+    switch (v) {
+#define GX_CASE(X) \
+    case X: return k_expand_flat<X>;
+        GX_CASE(1) GX_CASE(2) GX_CASE(3) GX_CASE(4) GX_CASE(5) GX_CASE(6) GX_CASE(7) GX_CASE(8)
+        GX_CASE(9) GX_CASE(10) GX_CASE(11) GX_CASE(12) GX_CASE(13) GX_CASE(14) GX_CASE(15)
+        GX_CASE(16)
+#undef GX_CASE
+    }
+    return nullptr;
+}
+
+// FINDORPUT + append of INSERTED keys (the receive side of the exchange)
+template <int BW, int V, int G, bool MARK>
+__global__ void __launch_bounds__(256) k_insert_append(TableDesc T, const uint32_t* __restrict__ keys,
+                                                       uint64_t n, uint32_t* out, uint64_t cap,
+                                                       unsigned long long* ctr) {
+    // ctr: [0] appended, [1] table full, [2] overflow
+    const int lane = threadIdx.x & 31;
+    constexpr int R = MARK ? 32 / G : 32;
+    const int grp = MARK ? lane / G : lane;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    for (uint64_t base = warp * R; base < n; base += nwarps * R) {
+        const uint64_t e = base + grp;
+        const bool active = e < n;
+        uint32_t key[V];
+#pragma unroll
+        for (int w = 0; w < V; w++) key[w] = active ? keys[e * V + w] : 0u;
+        const uint64_t h = fold<V>(T.salt, key);
+        int64_t hd;
+        int code;
+        bool leader;
+        if constexpr (MARK) {
+            code = probe_mark<BW, V, G>(T, active, key, h, &hd);
+            leader = active && (lane & (G - 1)) == 0;
+        } else {
+            code = active ? probe_status(T, key, h, &hd) : FOUND;
+            leader = active;
+        }
+        const bool ins = leader && code == INSERTED;
+        if (__any_sync(FULLMASK, leader && code == TABLE_FULL) && lane == 0) atomicExch(&ctr[1], 1ull);
+        const uint32_t insm = __ballot_sync(FULLMASK, ins);
+        if (insm) {
+            unsigned long long pos0 = 0;
+            if (lane == 0) pos0 = atomicAdd(&ctr[0], (unsigned long long)__popc(insm));
+            pos0 = __shfl_sync(FULLMASK, pos0, 0);
+            if (ins) {
+                const unsigned long long p = pos0 + __popc(insm & lanemask_lt());
+                if (p < cap)
+                    store_state<V>(out + p * V, key);
+                else
+                    atomicExch(&ctr[2], 1ull);
+            }
+        }
+    }
+}
+
+typedef void (*append_kernel_t)(TableDesc, const uint32_t*, uint64_t, uint32_t*, uint64_t,
+                                unsigned long long*);
+
+template <int BW, int V>
+static append_kernel_t pick_append_g(int g) {
+    switch (g) {
+        case 1: return k_insert_append<BW, V, 1, true>;
+        case 2: if (BW >= 8) return k_insert_append<BW, V, (BW >= 8 ? 2 : 1), true>; break;
+        case 4: if (BW >= 16) return k_insert_append<BW, V, (BW >= 16 ? 4 : 1), true>; break;
+        case 8: if (BW >= 32) return k_insert_append<BW, V, (BW >= 32 ? 8 : 1), true>; break;
+    }
+    return nullptr;
+}
+
+template <int BW>
+static append_kernel_t pick_append_v(int v, int g) {
+    switch (v) {
+        case 1: return pick_append_g<BW, 1>(g);
+        case 2: return pick_append_g<BW, 2>(g);
+        case 4: return pick_append_g<BW, 4>(g);
+    }
+    return nullptr;
+}
+
+static append_kernel_t pick_append(const TableDesc& T, int group) {
+    if (T.mode == MODE_STATUS) {
+        switch (T.vlen) {
+#define GX_CASE(X) \
+    case X: return k_insert_append<0, X, 1, false>;
+            GX_CASE(1) GX_CASE(2) GX_CASE(3) GX_CASE(4) GX_CASE(5) GX_CASE(6) GX_CASE(7) GX_CASE(8)
+            GX_CASE(9) GX_CASE(10) GX_CASE(11) GX_CASE(12) GX_CASE(13) GX_CASE(14) GX_CASE(15)
+            GX_CASE(16)
+#undef GX_CASE
+        }
+        return nullptr;
+    }
+    const int g = group > 0 ? group : default_group((int)T.bw);
+    switch (T.bw) {
+        case 4: return pick_append_v<4>((int)T.vlen, g);
+        case 8: return pick_append_v<8>((int)T.vlen, g);
+        case 16: return pick_append_v<16>((int)T.vlen, g);
+        case 32: return pick_append_v<32>((int)T.vlen, g);
+    }
+    return nullptr;
+}
+
+// ------------------------------------------------------------ benchmark
+
+// bijection on [0, 2^bits), keyed
+__device__ __forceinline__ uint64_t perm_bits(uint64_t x, int bits, uint64_t key) {
+    const uint64_t mask = bits >= 64 ? ~0ull : ((1ull << bits) - 1);
+    const int sh = bits / 2 + 1;
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        x = (x * (0x9E3779B97F4A7C15ull | 1ull)) & mask;
+        x ^= x >> sh;
+        x = (x + (key * (2 * r + 1) ^ (0xD6E8FEB86659FD93ull >> r))) & mask;
+        x ^= x >> (sh > 3 ? sh - 2 : 1);
+    }
+    return x & mask;
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// unique row r -> key words (injective in r for r < 2^(2*kb))
+template <int V>
+__device__ __forceinline__ void bench_row(uint64_t r, int kb, uint64_t seed, uint32_t* key) {
+    const uint64_t m = kb >= 32 ? 0xffffffffull : ((1ull << kb) - 1);
+    key[0] = (uint32_t)perm_bits(r & m, kb, seed);
+    if (V >= 2) key[1] = (uint32_t)((perm_bits((r >> kb) & m, kb, seed ^ 0x5bd1e995ull) ^ mix64(key[0] + seed)) & m);
+#pragma unroll
+    for (int w = 2; w < V; w++) key[w] = (uint32_t)(mix64(r * 0x9E3779B97F4A7C15ull + w + seed) & m);
+}
+
+struct BenchArgs {
+    uint64_t total, dup, unique, row_base, seed;
+    int32_t key_bits, perm_bits_n;
+    unsigned long long* ctr;  // [0] inserted, [1] full
+};
+
+template <int BW, int V, int G, bool MARK>
+__global__ void __launch_bounds__(256) k_bench(TableDesc T, BenchArgs B) {
+    const int lane = threadIdx.x & 31;
+    constexpr int R = MARK ? 32 / G : 32;
+    const int grp = MARK ? lane / G : lane;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    unsigned long long ins = 0, full = 0;
+    for (uint64_t base = warp * R; base < B.total; base += nwarps * R) {
+        const uint64_t e = base + grp;
+        const bool active = e < B.total;
+        uint32_t key[V];
+        if (active) {
+            uint64_t p = e;
+            do {
+                p = perm_bits(p, B.perm_bits_n, B.seed);
+            } while (p >= B.total);
+            uint64_t row = p / B.dup;
+            if (row >= B.unique) row = B.unique - 1;
+            bench_row<V>(row + B.row_base, B.key_bits, B.seed, key);
+        } else {
+#pragma unroll
+            for (int w = 0; w < V; w++) key[w] = 0;
+        }
+        const uint64_t h = fold<V>(T.salt, key);
+        int64_t hd;
+        int code;
+        bool leader;
+        if constexpr (MARK) {
+            code = probe_mark<BW, V, G>(T, active, key, h, &hd);
+            leader = active && (lane & (G - 1)) == 0;
+        } else {
+            code = active ? probe_status(T, key, h, &hd) : FOUND;
+            leader = active;
+        }
+        ins += leader && code == INSERTED;
+        full += leader && code == TABLE_FULL;
+    }
+    ins = warp_sum(ins);
+    full = warp_sum(full);
+    if (lane == 0) {
+        if (ins) atomicAdd(&B.ctr[0], ins);
+        if (full) atomicAdd(&B.ctr[1], full);
+    }
+}
+
+typedef void (*bench_kernel_t)(TableDesc, BenchArgs);
+
+template <int BW, int V>
+static bench_kernel_t pick_bench_g(int g) {
+    switch (g) {
+        case 1: return k_bench<BW, V, 1, true>;
+        case 2: if (BW >= 8) return k_bench<BW, V, (BW >= 8 ? 2 : 1), true>; break;
+        case 4: if (BW >= 16) return k_bench<BW, V, (BW >= 16 ? 4 : 1), true>; break;
+        case 8: if (BW >= 32) return k_bench<BW, V, (BW >= 32 ? 8 : 1), true>; break;
+    }
+    return nullptr;
+}
+
+template <int BW>
+static bench_kernel_t pick_bench_v(int v, int g) {
+    switch (v) {
+        case 1: return pick_bench_g<BW, 1>(g);
+        case 2: return pick_bench_g<BW, 2>(g);
+        case 4: return pick_bench_g<BW, 4>(g);
+    }
+    return nullptr;
+}
+
+static bench_kernel_t pick_bench(const TableDesc& T, int group) {
+    if (T.mode == MODE_STATUS) {
+        switch (T.vlen) {
+            case 1: return k_bench<0, 1, 1, false>;
+            case 2: return k_bench<0, 2, 1, false>;
+            case 3: return k_bench<0, 3, 1, false>;
+            case 4: return k_bench<0, 4, 1, false>;
+        }
+        return nullptr;
+    }
+    const int g = group > 0 ? group : default_group((int)T.bw);
+    switch (T.bw) {
+        case 4: return pick_bench_v<4>((int)T.vlen, g);
+        case 8: return pick_bench_v<8>((int)T.vlen, g);
+        case 16: return pick_bench_v<16>((int)T.vlen, g);
+        case 32: return pick_bench_v<32>((int)T.vlen, g);
+    }
+    return nullptr;
+}
+
+static int persistent_grid() { return sm_count() * 8; }
+
+}  // namespace gx
+
+using namespace gx;
+
+// ===================================================================== C ABI
+
+extern "C" {
+
+int gx_net_create(const gx_network_csr* c, void* stream, gx_net** out) {
+    *out = nullptr;
+    if (c->vlen < 1 || c->vlen > GX_MAXV) {
+        set_error("vector length %u outside 1..%d", c->vlen, GX_MAXV);
+        return GX_EINPUT;
+    }
+    if (c->n_proc != 4ull * c->nproc || c->n_rules != 4ull * c->nrules || c->n_qtab % 4 ||
+        c->n_parts % 4 || c->n_rq % 2 || c->n_trig < 1 || c->n_dedup < 1) {
+        set_error("malformed network CSR (section sizes)");
+        return GX_EINPUT;
+    }
+    gx_net* n = new gx_net();
+    n->stream = (cudaStream_t)stream;
+    n->vlen = c->vlen;
+    n->nproc = c->nproc;
+    n->initial.assign(c->initial, c->initial + c->vlen);
+    n->proc_host.resize(c->nproc);
+    memcpy(n->proc_host.data(), c->proc, sizeof(uint32_t) * c->n_proc);
+    // one blob, each section 16-byte aligned
+    const uint32_t* src[9] = {c->proc, c->qtab, c->im_dst, c->trig, c->rules,
+                              c->parts, c->rq, c->rdst, c->dedup};
+    const uint64_t len[9] = {c->n_proc, c->n_qtab, c->n_im_dst, c->n_trig, c->n_rules,
+                             c->n_parts, c->n_rq, c->n_rdst, c->n_dedup};
+    uint64_t off[10];
+    off[0] = 0;
+    for (int i = 0; i < 9; i++) off[i + 1] = off[i] + ((len[i] + 3) & ~3ull) + 4;
+    std::vector<uint32_t> blob(off[9] + 4, 0u);
+    for (int i = 0; i < 9; i++)
+        if (len[i]) memcpy(blob.data() + off[i], src[i], sizeof(uint32_t) * len[i]);
+    cudaError_t e = cudaMalloc(&n->d_blob, sizeof(uint32_t) * blob.size());
+    if (e == cudaSuccess) e = cudaMalloc(&n->d_initial, sizeof(uint32_t) * 16);
+    if (e != cudaSuccess) {
+        set_error("network upload failed: %s", cudaGetErrorString(e));
+        delete n;
+        return GX_EINTERNAL;
+    }
+    GX_CUDA(cudaMemcpyAsync(n->d_blob, blob.data(), sizeof(uint32_t) * blob.size(),
+                            cudaMemcpyHostToDevice, n->stream));
+    GX_CUDA(cudaMemcpyAsync(n->d_initial, c->initial, sizeof(uint32_t) * c->vlen,
+                            cudaMemcpyHostToDevice, n->stream));
+    GX_CUDA(cudaStreamSynchronize(n->stream));
+    NetDesc& d = n->d;
+    d.proc = (const uint4*)(n->d_blob + off[0]);
+    d.qtab = (const uint4*)(n->d_blob + off[1]);
+    d.im_dst = n->d_blob + off[2];
+    d.trig = n->d_blob + off[3];
+    d.rules = (const uint4*)(n->d_blob + off[4]);
+    d.parts = (const uint4*)(n->d_blob + off[5]);
+    d.rq = (const uint2*)(n->d_blob + off[6]);
+    d.rdst = n->d_blob + off[7];
+    d.dedup = n->d_blob + off[8];
+    d.nproc = c->nproc;
+    d.nrules = c->nrules;
+    d.vlen = c->vlen;
+    *out = n;
+    return GX_OK;
+}
+
+int gx_net_destroy(gx_net* n) {
+    if (!n) return GX_OK;
+    cudaStreamSynchronize(n->stream);
+    cudaFree(n->d_blob);
+    cudaFree(n->d_initial);
+    n->scratch.release();
+    n->dl.release();
+    delete n;
+    return GX_OK;
+}
+
+int gx_expand(gx_net* n, const uint32_t* states, uint64_t ns, uint64_t* counts, uint32_t* nsucc,
+              uint32_t* succ, uint64_t cap, uint64_t* total) {
+    const uint64_t v = n->vlen;
+    if (ns == 0) {
+        if (total) *total = 0;
+        return GX_OK;
+    }
+    // scratch: states | counts | nsucc | offsets | out
+    const uint64_t b_states = sizeof(uint32_t) * ns * v, b_counts = 8 * ns, b_n = 4 * ns,
+                   b_offs = 8 * ns;
+    const uint64_t b_out = sizeof(uint32_t) * std::max<uint64_t>(cap, 1) * v;
+    int rc = n->scratch.ensure(b_states + b_counts + b_n + b_offs + b_out + 64);
+    if (rc) return rc;
+    char* base = (char*)n->scratch.p;
+    uint32_t* d_states = (uint32_t*)base;
+    unsigned long long* d_counts = (unsigned long long*)(base + ((b_states + 15) & ~15ull));
+    uint32_t* d_n = (uint32_t*)((char*)d_counts + b_counts);
+    unsigned long long* d_offs = (unsigned long long*)((char*)d_n + ((b_n + 15) & ~15ull));
+    uint32_t* d_out = (uint32_t*)((char*)d_offs + b_offs);
+    GX_CUDA(cudaMemcpyAsync(d_states, states, b_states, cudaMemcpyHostToDevice, n->stream));
+    pick_count((int)v)<<<(int)((ns + 127) / 128), 128, 0, n->stream>>>(n->d, d_states, ns, d_counts, d_n);
+    GX_LAUNCHED();
+    std::vector<unsigned long long> hc(ns);
+    std::vector<uint32_t> hn(ns);
+    GX_CUDA(cudaMemcpyAsync(hc.data(), d_counts, b_counts, cudaMemcpyDeviceToHost, n->stream));
+    GX_CUDA(cudaMemcpyAsync(hn.data(), d_n, b_n, cudaMemcpyDeviceToHost, n->stream));
+    GX_CUDA(cudaStreamSynchronize(n->stream));
+    std::vector<unsigned long long> offs(ns);
+    unsigned long long tot = 0;
+    for (uint64_t i = 0; i < ns; i++) {
+        offs[i] = tot;
+        tot += hn[i];
+        if (counts) counts[i] = hc[i];
+        if (nsucc) nsucc[i] = hn[i];
+    }
+    if (total) *total = tot;
+    if (succ && cap) {
+        GX_CUDA(cudaMemcpyAsync(d_offs, offs.data(), b_offs, cudaMemcpyHostToDevice, n->stream));
+        pick_emit((int)v)<<<(int)((ns + 127) / 128), 128, 0, n->stream>>>(n->d, d_states, ns, d_offs,
+                                                                          d_out, cap);
+        GX_LAUNCHED();
+        GX_CUDA(cudaMemcpyAsync(succ, d_out, sizeof(uint32_t) * std::min<uint64_t>(cap, tot) * v,
+                                cudaMemcpyDeviceToHost, n->stream));
+        GX_CUDA(cudaStreamSynchronize(n->stream));
+    }
+    return GX_OK;
+}
+
+// composite-order comparison of two packed vectors (unpack, then
+// lexicographic over processes: sorted() of state tuples, explore.py:361-367)
+static bool composite_less(const gx_net* n, const uint32_t* a, const uint32_t* b) {
+    for (uint32_t i = 0; i < n->nproc; i++) {
+        const uint4 p = n->proc_host[i];
+        const uint32_t x = (a[p.x] >> p.y) & p.z, y = (b[p.x] >> p.y) & p.z;
+        if (x != y) return x < y;
+    }
+    return false;
+}
+
+static void keep_smallest(const gx_net* n, std::vector<uint32_t>& kept, const uint32_t* add,
+                          uint64_t cnt) {
+    const uint32_t v = n->vlen;
+    const uint64_t have = kept.size() / v;
+    std::vector<uint64_t> idx(have + cnt);
+    std::vector<uint32_t> all(kept);
+    all.insert(all.end(), add, add + cnt * v);
+    for (uint64_t i = 0; i < idx.size(); i++) idx[i] = i;
+    std::sort(idx.begin(), idx.end(), [&](uint64_t x, uint64_t y) {
+        return composite_less(n, all.data() + x * v, all.data() + y * v);
+    });
+    const uint64_t keep = std::min<uint64_t>(idx.size(), GX_DEADLOCK_KEEP);
+    kept.resize(keep * v);
+    for (uint64_t i = 0; i < keep; i++)
+        memcpy(kept.data() + i * v, all.data() + idx[i] * v, sizeof(uint32_t) * v);
+}
+
+int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep, uint32_t* deadlocks) {
+    memset(rep, 0, sizeof *rep);
+    const TableDesc& T = t->d;
+    const uint32_t v = n->vlen;
+    if (T.vlen != v) {
+        set_error("table vector length %u != network vector length %u", T.vlen, v);
+        return GX_EINPUT;
+    }
+    cudaStream_t st = t->stream;
+    const uint64_t launches0 = gx_kernel_launches();
+    level_kernel_t lk = pick_level(T, cfg->probe_group);
+    if (!lk) {
+        set_error("no level kernel for bw=%u vlen=%u group=%d", T.bw, v, cfg->probe_group);
+        return GX_EINPUT;
+    }
+    int rc = gx_table_clear(t);
+    if (rc) return rc;
+    // frontier buffer: two-ended, capacity C vectors
+    uint64_t C = cfg->frontier_capacity;
+    if (C == 0) {
+        size_t fr = 0, tot = 0;
+        GX_CUDA(cudaMemGetInfo(&fr, &tot));
+        const uint64_t reserve = 512ull << 20;
+        uint64_t avail = fr > reserve + t->aux2.bytes ? fr - reserve + t->aux2.bytes : (64ull << 20);
+        C = std::min<uint64_t>(t->total_slots + 2, avail * 9 / 10 / (4ull * v));
+        if (C < 1024) C = 1024;
+    }
+    rc = t->aux2.ensure(sizeof(uint32_t) * C * v);
+    if (rc) return rc;
+    uint32_t* fb = (uint32_t*)t->aux2.p;
+    const uint64_t dl_cap = 1 << 16;
+    rc = n->dl.ensure(sizeof(uint32_t) * dl_cap * v);
+    if (rc) return rc;
+    cudaEvent_t e0, e1;
+    GX_CUDA(cudaEventCreate(&e0));
+    GX_CUDA(cudaEventCreate(&e1));
+    GX_CUDA(cudaEventRecord(e0, st));
+    // initial state (explore.py:311-315)
+    rc = t->codes.ensure(16);
+    if (rc) return rc;
+    rc = table_find_or_put_dev(t, n->d_initial, 1, (uint8_t*)t->codes.p, nullptr, 0, cfg->probe_group);
+    if (rc) return rc;
+    GX_CUDA(cudaMemcpyAsync(fb, n->d_initial, sizeof(uint32_t) * v, cudaMemcpyDeviceToDevice, st));
+    uint8_t code0 = 0;
+    GX_CUDA(cudaMemcpyAsync(&code0, t->codes.p, 1, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    unsigned long long* ctr = (unsigned long long*)t->d_ctr;
+    unsigned long long* hc = (unsigned long long*)t->h_ctr;
+    std::vector<uint32_t> kept;
+    std::vector<uint32_t> dlhost;
+    uint64_t rounds = 0, states = 0, max_front = 0;
+    int outcome = GX_COMPLETE;
+    const uint32_t* pending = nullptr;  // last produced, unexpanded frontier
+    uint64_t n_pending = 0;
+    if (code0 == TABLE_FULL) {
+        outcome = GX_OUTCOME_TABLE_FULL;
+    } else {
+        states = 1;
+        // F at the left end, F' grows from the right end (and vice versa)
+        const uint32_t* F = fb;
+        uint64_t nF = 1;
+        int rev = 1;
+        unsigned long long new_base = 0, dl_base = 0;
+        const int grid = persistent_grid();
+        for (;;) {
+            const uint64_t claims = nF;
+            max_front = std::max<uint64_t>(max_front, nF);
+            uint64_t nnew = 0;
+            const uint32_t* Fn = nullptr;
+            if (claims) {
+                LevelArgs A;
+                A.front = F;
+                A.nfront = nF;
+                A.out = fb;
+                A.out_cap = C;
+                A.out_limit = C - nF;
+                A.out_rev = rev;
+                A.detect = cfg->detect_deadlocks;
+                A.ctr = ctr;
+                A.new_base = new_base;
+                A.dl_base = dl_base;
+                A.dl = (uint32_t*)n->dl.p;
+                A.dl_cap = dl_cap;
+                const uint64_t want = (nF + 31) / 32;  // warps
+                const int g = (int)std::min<uint64_t>((uint64_t)grid, (want + 7) / 8);
+                lk<<<g, 256, 0, st>>>(T, n->d, A);
+                GX_LAUNCHED();
+                rep->levels_launched++;
+            }
+            GX_CUDA(cudaMemcpyAsync(hc, ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost, st));
+            GX_CUDA(cudaStreamSynchronize(st));
+            nnew = hc[LV_NEW] - new_base;
+            new_base = hc[LV_NEW];
+            if (hc[LV_DL] > dl_base) {
+                const uint64_t d = std::min<uint64_t>(hc[LV_DL] - dl_base, dl_cap);
+                dlhost.resize(d * v);
+                GX_CUDA(cudaMemcpyAsync(dlhost.data(), n->dl.p, sizeof(uint32_t) * d * v,
+                                        cudaMemcpyDeviceToHost, st));
+                GX_CUDA(cudaStreamSynchronize(st));
+                keep_smallest(n, kept, dlhost.data(), d);
+                dl_base = hc[LV_DL];
+            }
+            if (hc[LV_OVF]) {
+                set_error("frontier capacity (%llu vectors) exceeded; raise frontier_capacity",
+                          (unsigned long long)C);
+                cudaEventDestroy(e0);
+                cudaEventDestroy(e1);
+                return GX_EINTERNAL;
+            }
+            states += nnew;
+            Fn = rev ? fb + (C - nnew) * v : fb;
+            rounds++;
+            pending = Fn;
+            n_pending = nnew;
+            if (hc[LV_FULL]) {
+                outcome = GX_OUTCOME_TABLE_FULL;
+                break;
+            }
+            if (claims == 0) break;
+            if (cfg->max_iterations > 0 && rounds >= (uint64_t)cfg->max_iterations) {
+                outcome = GX_ITERATION_CAP;
+                break;
+            }
+            F = Fn;
+            nF = nnew;
+            rev ^= 1;
+        }
+    }
+    GX_CUDA(cudaEventRecord(e1, st));
+    // statuses as the reference leaves them: OLD except the unexpanded level
+    rc = table_fixup_status(t, pending, n_pending);
+    if (rc) return rc;
+    GX_CUDA(cudaMemcpyAsync(hc, ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    GX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    // occupancy counters of the table after the run
+    unsigned long long cset[2] = {states, states - n_pending};
+    GX_CUDA(cudaMemcpyAsync(ctr, cset, sizeof cset, cudaMemcpyHostToDevice, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    rep->states = states;
+    rep->transitions = hc[LV_TRANS];
+    rep->expanded = hc[LV_EXP];
+    rep->iterations = rounds;
+    rep->deadlocks_total = hc[LV_DL];
+    rep->outcome = outcome;
+    rep->deadlocks_kept = (int32_t)(kept.size() / v);
+    if (deadlocks && !kept.empty()) memcpy(deadlocks, kept.data(), sizeof(uint32_t) * kept.size());
+    rep->device_ms = ms;
+    rep->max_frontier = max_front;
+    rep->kernels = gx_kernel_launches() - launches0;
+    return GX_OK;
+}
+
+int gx_expand_route(gx_net* n, const gx_table* t, const uint32_t* d_front, uint64_t nfront,
+                    int32_t ranks, uint32_t* d_out, uint64_t cap, uint64_t* d_counts,
+                    uint64_t* d_offsets, uint64_t* transitions, uint64_t* deadlocks,
+                    int32_t detect) {
+    const uint32_t v = n->vlen;
+    if (ranks < 1) {
+        set_error("ranks must be >= 1");
+        return GX_EINPUT;
+    }
+    cudaStream_t st = n->stream;
+    if (ranks > 64) {
+        set_error("at most 64 ranks");
+        return GX_EINPUT;
+    }
+    // scratch: counters (8) + cursors (64) | flat successors (cap)
+    const uint64_t head = 8 * 72;
+    int rc = n->scratch.ensure(head + sizeof(uint32_t) * std::max<uint64_t>(cap, 1) * v);
+    if (rc) return rc;
+    unsigned long long* c = (unsigned long long*)n->scratch.p;
+    uint32_t* flat = (uint32_t*)((char*)n->scratch.p + head);
+    const uint64_t dl_cap = 1 << 16;
+    rc = n->dl.ensure(sizeof(uint32_t) * dl_cap * v);
+    if (rc) return rc;
+    GX_CUDA(cudaMemsetAsync(c, 0, 64, st));
+    unsigned long long h[8] = {0};
+    if (nfront) {
+        const int g = (int)std::min<uint64_t>((uint64_t)persistent_grid(), (nfront + 255) / 256);
+        pick_flat((int)v)<<<g, 256, 0, st>>>(n->d, d_front, nfront, flat, cap, c, (uint32_t*)n->dl.p,
+                                            dl_cap, detect);
+        GX_LAUNCHED();
+    }
+    GX_CUDA(cudaMemcpyAsync(h, c, 64, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    if (h[3]) {
+        set_error("successor buffer capacity (%llu vectors) exceeded", (unsigned long long)cap);
+        return GX_EINTERNAL;
+    }
+    const uint64_t nsucc = h[0];
+    GX_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(uint64_t) * ranks, st));
+    if (nsucc) {
+        k_owner_hist<<<(int)((nsucc + 255) / 256), 256, 0, st>>>(t->d.salt, flat, nsucc, (int)v, ranks,
+                                                                (unsigned long long*)d_counts);
+        GX_LAUNCHED();
+    }
+    std::vector<unsigned long long> cnt(ranks), offs(ranks);
+    GX_CUDA(cudaMemcpyAsync(cnt.data(), d_counts, sizeof(uint64_t) * ranks, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    unsigned long long acc = 0;
+    for (int r = 0; r < ranks; r++) {
+        offs[r] = acc;
+        acc += cnt[r];
+    }
+    GX_CUDA(cudaMemcpyAsync(d_offsets, offs.data(), sizeof(uint64_t) * ranks, cudaMemcpyHostToDevice, st));
+    if (nsucc) {
+        unsigned long long* d_cur = c + 8;  // scatter cursors start at the offsets
+        GX_CUDA(cudaMemcpyAsync(d_cur, offs.data(), sizeof(unsigned long long) * ranks,
+                                cudaMemcpyHostToDevice, st));
+        k_owner_scatter<<<(int)((nsucc + 255) / 256), 256, 0, st>>>(t->d.salt, flat, nsucc, (int)v, ranks,
+                                                                   d_cur, d_out);
+        GX_LAUNCHED();
+        GX_CUDA(cudaStreamSynchronize(st));
+    }
+    if (transitions) *transitions = h[1];
+    if (deadlocks) *deadlocks = h[2];
+    n->dl_recorded = std::min<uint64_t>(h[2], dl_cap);
+    return GX_OK;
+}
+
+int gx_net_deadlocks(gx_net* n, uint32_t* out, uint64_t cap, uint64_t* count) {
+    const uint64_t k = std::min<uint64_t>(n->dl_recorded, cap);
+    if (count) *count = n->dl_recorded;
+    if (out && k) {
+        GX_CUDA(cudaMemcpyAsync(out, n->dl.p, sizeof(uint32_t) * k * n->vlen, cudaMemcpyDeviceToHost,
+                                n->stream));
+        GX_CUDA(cudaStreamSynchronize(n->stream));
+    }
+    return GX_OK;
+}
+
+int gx_insert_append(gx_table* t, const uint32_t* d_keys, uint64_t n, uint32_t* d_next, uint64_t cap,
+                     uint64_t* n_next, int32_t* table_full) {
+    append_kernel_t k = pick_append(t->d, 0);
+    if (!k) {
+        set_error("no append kernel for bw=%u vlen=%u", t->d.bw, t->d.vlen);
+        return GX_EINPUT;
+    }
+    cudaStream_t st = t->stream;
+    unsigned long long* c = (unsigned long long*)t->d_ctr + CTR_SCRATCH;  // cells 3..5
+    GX_CUDA(cudaMemsetAsync(c, 0, 3 * sizeof(unsigned long long), st));
+    if (n) {
+        const int g = (int)std::min<uint64_t>((uint64_t)persistent_grid(), (n + 255) / 256 + 1);
+        k<<<g, 256, 0, st>>>(t->d, d_keys, n, d_next, cap, c);
+        GX_LAUNCHED();
+    }
+    unsigned long long h[3];
+    GX_CUDA(cudaMemcpyAsync(h, c, sizeof h, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    if (h[2]) {
+        set_error("next-frontier capacity (%llu vectors) exceeded", (unsigned long long)cap);
+        return GX_EINTERNAL;
+    }
+    // keep occupancy in step
+    unsigned long long occ[1];
+    GX_CUDA(cudaMemcpyAsync(occ, t->d_ctr + CTR_OCCUPIED, 8, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    occ[0] += h[0];
+    GX_CUDA(cudaMemcpyAsync(t->d_ctr + CTR_OCCUPIED, occ, 8, cudaMemcpyHostToDevice, st));
+    if (n_next) *n_next = h[0];
+    if (table_full) *table_full = h[1] ? 1 : 0;
+    return GX_OK;
+}
+
+int gx_owner_of(const gx_table* t, const uint32_t* keys, uint64_t n, int32_t ranks, int32_t* owner) {
+    if (n == 0) return GX_OK;
+    const uint32_t v = t->d.vlen;
+    uint32_t* dk = nullptr;
+    int32_t* dout = nullptr;
+    GX_CUDA(cudaMalloc(&dk, sizeof(uint32_t) * n * v));
+    GX_CUDA(cudaMalloc(&dout, sizeof(int32_t) * n));
+    GX_CUDA(cudaMemcpy(dk, keys, sizeof(uint32_t) * n * v, cudaMemcpyHostToDevice));
+    k_owner_of<<<(int)((n + 255) / 256), 256>>>(t->d.salt, dk, n, (int)v, ranks, dout);
+    GX_LAUNCHED();
+    GX_CUDA(cudaMemcpy(owner, dout, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    cudaFree(dk);
+    cudaFree(dout);
+    return GX_OK;
+}
+
+int gx_bench_find_or_put(gx_table* t, uint64_t total, uint64_t dup, uint64_t seed, int32_t key_bits,
+                         int32_t group, double* ms, uint64_t* found, uint64_t* inserted,
+                         uint64_t* full) {
+    return gx_bench_find_or_put_rows(t, total, dup, 0, seed, key_bits, group, ms, found, inserted, full);
+}
+
+int gx_bench_find_or_put_rows(gx_table* t, uint64_t total, uint64_t dup, uint64_t row_base,
+                              uint64_t seed, int32_t key_bits, int32_t group, double* ms,
+                              uint64_t* found, uint64_t* inserted, uint64_t* full) {
+    if (total == 0 || dup == 0 || dup > total || key_bits < 1 || key_bits > 32) {
+        set_error("bad benchmark parameters");
+        return GX_EINPUT;
+    }
+    const TableDesc& T = t->d;
+    if (T.mode == MODE_MARK && key_bits > 31) {
+        set_error("table in mark mode stores keys of at most 31 bits per word");
+        return GX_EINPUT;
+    }
+    const uint64_t unique = total / dup;
+    if (T.vlen == 1 && unique + row_base > (1ull << key_bits)) {
+        set_error("%llu unique one-word keys do not fit in %d bits", (unsigned long long)unique, key_bits);
+        return GX_EINPUT;
+    }
+    bench_kernel_t k = pick_bench(T, group);
+    if (!k) {
+        set_error("no benchmark kernel for bw=%u vlen=%u group=%d", T.bw, T.vlen, group);
+        return GX_EINPUT;
+    }
+    cudaStream_t st = t->stream;
+    unsigned long long* c = (unsigned long long*)t->d_ctr + CTR_SCRATCH;
+    GX_CUDA(cudaMemsetAsync(c, 0, 2 * sizeof(unsigned long long), st));
+    BenchArgs B;
+    B.total = total;
+    B.dup = dup;
+    B.unique = unique;
+    B.row_base = row_base;
+    B.seed = seed;
+    B.key_bits = key_bits;
+    int pb = 1;
+    while ((1ull << pb) < total) pb++;
+    B.perm_bits_n = pb;
+    B.ctr = c;
+    cudaEvent_t e0, e1;
+    GX_CUDA(cudaEventCreate(&e0));
+    GX_CUDA(cudaEventCreate(&e1));
+    GX_CUDA(cudaEventRecord(e0, st));
+    k<<<persistent_grid(), 256, 0, st>>>(T, B);
+    GX_LAUNCHED();
+    GX_CUDA(cudaEventRecord(e1, st));
+    unsigned long long h[2];
+    GX_CUDA(cudaMemcpyAsync(h, c, sizeof h, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    float f = 0;
+    GX_CUDA(cudaEventElapsedTime(&f, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    // occupancy bookkeeping
+    unsigned long long occ;
+    GX_CUDA(cudaMemcpy(&occ, t->d_ctr + CTR_OCCUPIED, 8, cudaMemcpyDeviceToHost));
+    occ += h[0];
+    GX_CUDA(cudaMemcpy(t->d_ctr + CTR_OCCUPIED, &occ, 8, cudaMemcpyHostToDevice));
+    if (ms) *ms = f;
+    if (inserted) *inserted = h[0];
+    if (full) *full = h[1];
+    if (found) *found = total - h[0] - h[1];
+    return GX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,696 @@
+// gx_table.cu -- the B200 state table: creation, batch FINDORPUT, claim,
+// scan/compaction, occupancy and inspection (reference: hashtable.py).
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <mutex>
+
+#include "gx_internal.h"
+
+namespace gx {
+
+static thread_local char g_err[1024];
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+
+void count_launch(uint64_t n) { g_launches += n; }
+
+int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+            sms = 148;
+    }
+    return sms;
+}
+
+static uint64_t splitmix_next(uint64_t* x) {
+    *x += 0x9E3779B97F4A7C15ull;
+    uint64_t z = *x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+    return __reduce_add_sync(FULLMASK, v);
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+    return v;
+}
+
+// --------------------------------------------------------- FINDORPUT batch
+
+template <int BW, int V, int G>
+__global__ void __launch_bounds__(256) k_fop_mark(TableDesc T, const uint32_t* __restrict__ keys,
+                                                  uint64_t n, uint8_t* codes, int64_t* handles,
+                                                  unsigned long long* ctr, int serial) {
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / G;
+    const int R = serial ? 1 : 32 / G;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    unsigned long long ins = 0, full = 0;
+    for (uint64_t base = warp * R; base < n; base += nwarps * R) {
+        const uint64_t e = base + grp;
+        const bool active = grp < R && e < n;
+        uint32_t key[V];
+#pragma unroll
+        for (int w = 0; w < V; w++) key[w] = active ? keys[e * V + w] : 0u;
+        const uint64_t h = fold<V>(T.salt, key);
+        int64_t hd;
+        const int code = probe_mark<BW, V, G>(T, active, key, h, &hd);
+        if (active && (lane & (G - 1)) == 0) {
+            if (codes) codes[e] = (uint8_t)code;
+            if (handles) handles[e] = hd;
+            ins += code == INSERTED;
+            full += code == TABLE_FULL;
+        }
+    }
+    ins = warp_sum_u64(ins);
+    full = warp_sum_u64(full);
+    if (lane == 0) {
+        if (ins) atomicAdd(&ctr[CTR_OCCUPIED], ins);
+        if (full) atomicAdd(&ctr[CTR_FULL], full);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_fop_status(TableDesc T, const uint32_t* __restrict__ keys,
+                                                    uint64_t n, uint8_t* codes, int64_t* handles,
+                                                    unsigned long long* ctr, int serial) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nth = serial ? 1 : gridDim.x * (uint64_t)blockDim.x;
+    unsigned long long ins = 0, full = 0;
+    uint32_t key[GX_MAXV];
+    if (!serial || tid == 0) {
+        for (uint64_t e = tid; e < n; e += nth) {
+            for (int w = 0; w < (int)T.vlen; w++) key[w] = keys[e * T.vlen + w];
+            const uint64_t h = fold_rt(T.salt, key, (int)T.vlen);
+            int64_t hd;
+            const int code = probe_status(T, key, h, &hd);
+            if (codes) codes[e] = (uint8_t)code;
+            if (handles) handles[e] = hd;
+            ins += code == INSERTED;
+            full += code == TABLE_FULL;
+        }
+    }
+    ins = warp_sum_u64(ins);
+    full = warp_sum_u64(full);
+    if ((threadIdx.x & 31) == 0) {
+        if (ins) atomicAdd(&ctr[CTR_OCCUPIED], ins);
+        if (full) atomicAdd(&ctr[CTR_FULL], full);
+    }
+}
+
+typedef void (*fop_kernel_t)(TableDesc, const uint32_t*, uint64_t, uint8_t*, int64_t*,
+                             unsigned long long*, int);
+
+template <int BW, int V>
+static fop_kernel_t pick_g(int g) {
+    switch (g) {
+        case 1: return k_fop_mark<BW, V, 1>;
+        case 2: if (BW >= 8) return k_fop_mark<BW, V, (BW >= 8 ? 2 : 1)>; break;
+        case 4: if (BW >= 16) return k_fop_mark<BW, V, (BW >= 16 ? 4 : 1)>; break;
+        case 8: if (BW >= 32) return k_fop_mark<BW, V, (BW >= 32 ? 8 : 1)>; break;
+    }
+    return nullptr;
+}
+
+template <int BW>
+static fop_kernel_t pick_v(int v, int g) {
+    switch (v) {
+        case 1: return pick_g<BW, 1>(g);
+        case 2: return pick_g<BW, 2>(g);
+        case 4: return (BW >= 4) ? pick_g<BW, 4>(g) : nullptr;
+    }
+    return nullptr;
+}
+
+// default probe group: one 16-byte chunk per lane (a bucket per G lanes)
+int default_group(int bw) { return bw / 4; }
+
+static fop_kernel_t pick_fop(int bw, int v, int g) {
+    switch (bw) {
+        case 4: return pick_v<4>(v, g);
+        case 8: return pick_v<8>(v, g);
+        case 16: return pick_v<16>(v, g);
+        case 32: return pick_v<32>(v, g);
+    }
+    return nullptr;
+}
+
+static int grid_for(uint64_t items_per_block_round, uint64_t n) {
+    uint64_t want = (n + items_per_block_round - 1) / items_per_block_round;
+    uint64_t cap = (uint64_t)sm_count() * 8;
+    if (want < 1) want = 1;
+    return (int)std::min(want, cap);
+}
+
+int table_find_or_put_dev(gx_table* t, const uint32_t* d_keys, uint64_t n, uint8_t* d_codes,
+                          int64_t* d_handles, int serial, int group) {
+    if (n == 0) return GX_OK;
+    const TableDesc& T = t->d;
+    if (T.mode == MODE_MARK) {
+        int g = group > 0 ? group : default_group((int)T.bw);
+        fop_kernel_t k = pick_fop((int)T.bw, (int)T.vlen, g);
+        if (!k) {
+            set_error("no FINDORPUT kernel for bw=%u vlen=%u group=%d", T.bw, T.vlen, g);
+            return GX_EINPUT;
+        }
+        int grid = serial ? 1 : grid_for(256 / g, n);
+        k<<<grid, serial ? 32 : 256, 0, t->stream>>>(T, d_keys, n, d_codes, d_handles,
+                                                    (unsigned long long*)t->d_ctr, serial);
+    } else {
+        int grid = serial ? 1 : grid_for(256, n);
+        k_fop_status<<<grid, serial ? 32 : 256, 0, t->stream>>>(T, d_keys, n, d_codes, d_handles,
+                                                               (unsigned long long*)t->d_ctr, serial);
+    }
+    GX_LAUNCHED();
+    return GX_OK;
+}
+
+// ------------------------------------------------------------- slot state
+
+__device__ __forceinline__ uint32_t slot_status_of(const TableDesc& T, uint64_t bucket, int j) {
+    uint8_t b = T.status[bucket * (uint64_t)T.stride + j];
+    if (T.mode == MODE_STATUS) return b;
+    if (!slot_occupied(T, bucket, j)) return EMPTY;
+    return b == OLD ? OLD : NEW;
+}
+
+__device__ __forceinline__ void read_words(const TableDesc& T, uint64_t bucket, int j, uint32_t* out) {
+    const uint32_t* d = T.data + bucket * (uint64_t)T.bw + T.offsets[j];
+    for (int w = 0; w < (int)T.vlen; w++) {
+        uint32_t x = __ldcg(d + w);
+        if (T.mode == MODE_MARK && w == (int)T.mark_word) x &= ~T.mark;
+        out[w] = x;
+    }
+}
+
+// claim_new, hashtable.py:296-313.  In MODE_MARK an occupied slot's status
+// byte is 0 while NEW and OLD after the claim.
+__global__ void k_claim(TableDesc T, const int64_t* __restrict__ handles, uint64_t n, uint8_t* out,
+                        unsigned long long* ctr) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    unsigned long long won = 0;
+    if (i < n) {
+        const int64_t h = handles[i];
+        uint32_t ok = 0;
+        if (h >= 0 && (uint64_t)h < T.nb * T.spb) {
+            const uint64_t bucket = (uint64_t)h / T.spb;
+            const int j = (int)((uint64_t)h % T.spb);
+            uint8_t* cell = T.status + bucket * (uint64_t)T.stride + j;
+            uint32_t seen;
+            if (T.mode == MODE_STATUS)
+                ok = status_word_cas_byte(cell, NEW, OLD, &seen);
+            else if (slot_occupied(T, bucket, j))
+                ok = status_word_cas_byte(cell, 0u, OLD, &seen);
+        }
+        out[i] = (uint8_t)ok;
+        won = ok;
+    }
+    won = warp_sum_u64(won);
+    if ((threadIdx.x & 31) == 0 && won) atomicAdd(&ctr[CTR_OLD], won);
+}
+
+// Selection of slots in bucket-major order (scan_new / occupied dump):
+// each block owns a contiguous bucket range; pass 1 counts, the host scans
+// the block counts, pass 2 writes with a block-wide exclusive scan per
+// round of blockDim buckets so the output is globally sorted.
+enum { SEL_NEW = 0, SEL_OCCUPIED = 1 };
+
+__device__ __forceinline__ uint32_t select_mask(const TableDesc& T, uint64_t bucket, int pred) {
+    uint32_t m = 0;
+    for (int j = 0; j < (int)T.spb; j++) {
+        uint32_t st = slot_status_of(T, bucket, j);
+        bool sel = pred == SEL_NEW ? st == NEW : st >= NEW;
+        m |= (sel ? 1u : 0u) << j;
+    }
+    return m;
+}
+
+__global__ void __launch_bounds__(256) k_select_count(TableDesc T, uint64_t first, uint64_t last,
+                                                      uint64_t chunk, int pred,
+                                                      unsigned long long* blockcounts) {
+    const uint64_t lo = first + blockIdx.x * chunk;
+    const uint64_t hi = min(last, lo + chunk);
+    unsigned long long c = 0;
+    for (uint64_t b = lo + threadIdx.x; b < hi; b += blockDim.x) c += __popc(select_mask(T, b, pred));
+    c = warp_sum_u64(c);
+    __shared__ unsigned long long part[8];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += part[w];
+        blockcounts[blockIdx.x] = s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_select_write(TableDesc T, uint64_t first, uint64_t last,
+                                                      uint64_t chunk, int pred,
+                                                      const unsigned long long* blockoffs,
+                                                      uint64_t cap, int64_t* out_h, uint8_t* out_s,
+                                                      uint32_t* out_w) {
+    const uint64_t lo = first + blockIdx.x * chunk;
+    const uint64_t hi = min(last, lo + chunk);
+    __shared__ uint32_t wsum[8];
+    __shared__ unsigned long long running;
+    if (threadIdx.x == 0) running = blockoffs[blockIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (uint64_t b0 = lo; b0 < hi; b0 += blockDim.x) {
+        const uint64_t b = b0 + threadIdx.x;
+        const uint32_t m = b < hi ? select_mask(T, b, pred) : 0u;
+        const uint32_t c = __popc(m);
+        // block exclusive scan of c
+        uint32_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(FULLMASK, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[wid] = x;
+        __syncthreads();
+        uint32_t wpre = 0, total = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            if (w < wid) wpre += wsum[w];
+            total += wsum[w];
+        }
+        unsigned long long pos = running + wpre + x - c;
+        uint32_t mm = m;
+        while (mm) {
+            const int j = __ffs(mm) - 1;
+            mm &= mm - 1;
+            if (pos < cap) {
+                if (out_h) out_h[pos] = (int64_t)(b * T.spb + j);
+                if (out_s) out_s[pos] = (uint8_t)slot_status_of(T, b, j);
+                if (out_w) read_words(T, b, j, out_w + pos * T.vlen);
+            }
+            pos++;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) running += total;
+        __syncthreads();
+    }
+}
+
+static int select_slots(gx_table* t, uint64_t first, uint64_t last, int pred, int64_t* h_out,
+                        uint8_t* s_out, uint32_t* w_out, uint64_t cap, uint64_t* count) {
+    const TableDesc& T = t->d;
+    if (last > T.nb) last = T.nb;
+    if (first >= last) {
+        *count = 0;
+        return GX_OK;
+    }
+    const uint64_t nbk = last - first;
+    uint64_t nblocks = std::min<uint64_t>((uint64_t)sm_count() * 4, (nbk + 255) / 256);
+    if (nblocks < 1) nblocks = 1;
+    const uint64_t chunk = (nbk + nblocks - 1) / nblocks;
+    nblocks = (nbk + chunk - 1) / chunk;
+    int rc = t->aux.ensure(sizeof(unsigned long long) * nblocks);
+    if (rc) return rc;
+    unsigned long long* d_bc = (unsigned long long*)t->aux.p;
+    k_select_count<<<(int)nblocks, 256, 0, t->stream>>>(T, first, last, chunk, pred, d_bc);
+    GX_LAUNCHED();
+    std::vector<unsigned long long> bc(nblocks);
+    GX_CUDA(cudaMemcpyAsync(bc.data(), d_bc, sizeof(unsigned long long) * nblocks,
+                            cudaMemcpyDeviceToHost, t->stream));
+    GX_CUDA(cudaStreamSynchronize(t->stream));
+    unsigned long long total = 0;
+    for (uint64_t i = 0; i < nblocks; i++) {
+        unsigned long long c = bc[i];
+        bc[i] = total;
+        total += c;
+    }
+    *count = total;
+    if ((!h_out && !s_out && !w_out) || total == 0) return GX_OK;
+    const uint64_t n = std::min<uint64_t>(total, cap);
+    GX_CUDA(cudaMemcpyAsync(d_bc, bc.data(), sizeof(unsigned long long) * nblocks,
+                            cudaMemcpyHostToDevice, t->stream));
+    rc = t->handles.ensure(sizeof(int64_t) * n);
+    if (rc) return rc;
+    rc = t->codes.ensure(n);
+    if (rc) return rc;
+    rc = t->keys.ensure(sizeof(uint32_t) * n * T.vlen);
+    if (rc) return rc;
+    k_select_write<<<(int)nblocks, 256, 0, t->stream>>>(
+        T, first, last, chunk, pred, d_bc, n, h_out ? (int64_t*)t->handles.p : nullptr,
+        s_out ? (uint8_t*)t->codes.p : nullptr, w_out ? (uint32_t*)t->keys.p : nullptr);
+    GX_LAUNCHED();
+    if (h_out)
+        GX_CUDA(cudaMemcpyAsync(h_out, t->handles.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost,
+                                t->stream));
+    if (s_out) GX_CUDA(cudaMemcpyAsync(s_out, t->codes.p, n, cudaMemcpyDeviceToHost, t->stream));
+    if (w_out)
+        GX_CUDA(cudaMemcpyAsync(w_out, t->keys.p, sizeof(uint32_t) * n * T.vlen,
+                                cudaMemcpyDeviceToHost, t->stream));
+    GX_CUDA(cudaStreamSynchronize(t->stream));
+    return GX_OK;
+}
+
+__global__ void k_read_slots(TableDesc T, const int64_t* __restrict__ handles, uint64_t n,
+                             uint8_t* st, uint32_t* words) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t h = handles[i];
+    if (h < 0 || (uint64_t)h >= T.nb * T.spb) {
+        if (st) st[i] = 0xff;
+        return;
+    }
+    const uint64_t bucket = (uint64_t)h / T.spb;
+    const int j = (int)((uint64_t)h % T.spb);
+    if (st) st[i] = (uint8_t)slot_status_of(T, bucket, j);
+    if (words) read_words(T, bucket, j, words + i * T.vlen);
+}
+
+// explore epilogue: every occupied slot OLD ...
+__global__ void k_mark_all_old(TableDesc T) {
+    const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < T.nb; b += stride) {
+        for (int j = 0; j < (int)T.spb; j++) {
+            if (slot_occupied(T, b, j)) T.status[b * (uint64_t)T.stride + j] = OLD;
+        }
+    }
+}
+
+// ... then the given handles NEW again
+__global__ void k_mark_new(TableDesc T, const int64_t* __restrict__ handles, uint64_t n) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t h = handles[i];
+    if (h < 0) return;
+    const uint64_t bucket = (uint64_t)h / T.spb;
+    const int j = (int)((uint64_t)h % T.spb);
+    T.status[bucket * (uint64_t)T.stride + j] = T.mode == MODE_STATUS ? NEW : 0;
+}
+
+int table_fixup_status(gx_table* t, const uint32_t* d_new_keys, uint64_t n_new) {
+    const TableDesc& T = t->d;
+    int grid = (int)std::min<uint64_t>((uint64_t)sm_count() * 8, (T.nb + 255) / 256);
+    if (grid < 1) grid = 1;
+    k_mark_all_old<<<grid, 256, 0, t->stream>>>(T);
+    GX_LAUNCHED();
+    if (n_new) {
+        int rc = t->handles.ensure(sizeof(int64_t) * n_new);
+        if (rc) return rc;
+        // the keys are present: FINDORPUT returns FOUND with their handles
+        unsigned long long saved[CTR_N];
+        GX_CUDA(cudaMemcpyAsync(saved, t->d_ctr, sizeof saved, cudaMemcpyDeviceToHost, t->stream));
+        GX_CUDA(cudaStreamSynchronize(t->stream));
+        rc = table_find_or_put_dev(t, d_new_keys, n_new, nullptr, (int64_t*)t->handles.p, 0, 0);
+        if (rc) return rc;
+        k_mark_new<<<(int)((n_new + 255) / 256), 256, 0, t->stream>>>(T, (const int64_t*)t->handles.p,
+                                                                      n_new);
+        GX_LAUNCHED();
+        GX_CUDA(cudaMemcpyAsync(t->d_ctr, saved, sizeof saved, cudaMemcpyHostToDevice, t->stream));
+    }
+    return GX_OK;
+}
+
+}  // namespace gx
+
+using namespace gx;
+
+// ===================================================================== C ABI
+
+extern "C" {
+
+const char* gx_last_error(void) { return g_err; }
+
+uint64_t gx_kernel_launches(void) { return g_launches.load(); }
+
+int gx_device_info(int32_t* sms, uint64_t* free_b, uint64_t* total_b) {
+    size_t f = 0, tt = 0;
+    GX_CUDA(cudaMemGetInfo(&f, &tt));
+    if (sms) *sms = sm_count();
+    if (free_b) *free_b = f;
+    if (total_b) *total_b = tt;
+    return GX_OK;
+}
+
+int gx_sync(void* stream) {
+    GX_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return GX_OK;
+}
+
+// slots_per_bucket, hashtable.py:89-111
+static int spb_of(int bw, int vlen, int layout) {
+    if (bw <= 0 || vlen <= 0) {
+        set_error("bucket_words and vector_length must be positive");
+        return 0;
+    }
+    int c;
+    if (layout == GX_LAYOUT_HALF) {
+        if (bw % 2) {
+            set_error("half-bucket layout requires an even bucket size");
+            return 0;
+        }
+        c = 2 * ((bw / 2) / vlen);
+    } else if (layout == GX_LAYOUT_PLAIN) {
+        c = bw / vlen;
+    } else {
+        set_error("unknown layout %d", layout);
+        return 0;
+    }
+    if (c == 0) {
+        set_error("vector too long for bucket: %d words in a %d-word bucket (%s)", vlen, bw,
+                  layout == GX_LAYOUT_HALF ? "half" : "plain");
+        return 0;
+    }
+    return c;
+}
+
+int gx_table_create(const gx_table_cfg* cfg, void* stream, gx_table** out) {
+    *out = nullptr;
+    const int bw = cfg->bucket_words;
+    if (bw != 4 && bw != 8 && bw != 16 && bw != 32) {
+        set_error("bucket_words must be one of (4, 8, 16, 32), got %d", bw);
+        return GX_EINPUT;
+    }
+    if (cfg->num_hash_functions < 1) {
+        set_error("need at least one hash function");
+        return GX_EINPUT;
+    }
+    if (cfg->num_hash_functions > GX_MAXK) {
+        set_error("at most %d hash functions are supported, got %d", GX_MAXK, cfg->num_hash_functions);
+        return GX_EINPUT;
+    }
+    if (cfg->vector_length < 1 || cfg->vector_length > GX_MAXV) {
+        set_error("vector_length must be in 1..%d, got %d", GX_MAXV, cfg->vector_length);
+        return GX_EINPUT;
+    }
+    const int spb = spb_of(bw, cfg->vector_length, cfg->layout);
+    if (!spb) return GX_EINPUT;
+    const uint64_t nb = cfg->capacity_words / (uint64_t)bw;
+    if (nb < (uint64_t)cfg->num_hash_functions) {
+        set_error("capacity_words %llu gives %llu buckets, fewer than %d hash functions",
+                  (unsigned long long)cfg->capacity_words, (unsigned long long)nb,
+                  cfg->num_hash_functions);
+        return GX_EINPUT;
+    }
+    gx_table* t = new gx_table();
+    t->cfg = *cfg;
+    t->stream = (cudaStream_t)stream;
+    TableDesc& T = t->d;
+    memset(&T, 0, sizeof T);
+    T.nb = nb;
+    T.nb_magic = nb == 1 ? 0 : (uint64_t)(((unsigned __int128)1 << 64) / nb);
+    T.bw = (uint32_t)bw;
+    T.vlen = (uint32_t)cfg->vector_length;
+    T.spb = (uint32_t)spb;
+    T.stride = (uint32_t)((spb + 7) & ~7);
+    T.k = (uint32_t)cfg->num_hash_functions;
+    const int v = cfg->vector_length;
+    bool contiguous = true;
+    for (int j = 0; j < spb; j++) {
+        int off = (cfg->layout == GX_LAYOUT_HALF && j >= spb / 2) ? bw / 2 + (j - spb / 2) * v : j * v;
+        T.offsets[j] = (uint8_t)off;
+        if (off != j * v) contiguous = false;
+    }
+    const bool mark_ok = cfg->mark_word >= 0 && cfg->mark_word < v && cfg->mark_bit >= 0 &&
+                         cfg->mark_bit < 32 && (v == 1 || v == 2 || v == 4) && contiguous &&
+                         spb * v == bw;
+    T.mode = mark_ok ? MODE_MARK : MODE_STATUS;
+    T.mark_word = mark_ok ? (uint32_t)cfg->mark_word : 0;
+    T.mark = mark_ok ? (1u << cfg->mark_bit) : 0;
+    uint64_t x = cfg->seed;
+    for (int i = 0; i < cfg->num_hash_functions; i++) {
+        T.a[i] = splitmix_next(&x) | 1ull;
+        T.b[i] = splitmix_next(&x);
+    }
+    uint64_t y = cfg->seed ^ 0xA5A5A5A5A5A5A5A5ull;
+    T.salt = splitmix_next(&y);
+    t->total_slots = nb * (uint64_t)spb;
+    cudaError_t e1 = cudaMalloc(&T.data, nb * (uint64_t)bw * 4);
+    cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&T.status, nb * (uint64_t)T.stride) : e1;
+    cudaError_t e3 = e2 == cudaSuccess ? cudaMalloc(&t->d_ctr, sizeof(uint64_t) * CTR_N) : e2;
+    cudaError_t e4 = e3 == cudaSuccess ? cudaMallocHost(&t->h_ctr, sizeof(uint64_t) * CTR_N) : e3;
+    if (e4 != cudaSuccess) {
+        set_error("device allocation of a %llu-byte table failed: %s",
+                  (unsigned long long)(nb * (uint64_t)bw * 4 + nb * (uint64_t)T.stride),
+                  cudaGetErrorString(e4));
+        cudaGetLastError();
+        if (T.data) cudaFree(T.data);
+        if (T.status) cudaFree(T.status);
+        if (t->d_ctr) cudaFree(t->d_ctr);
+        delete t;
+        return GX_EINPUT;
+    }
+    int rc = gx_table_clear(t);
+    if (rc) {
+        gx_table_destroy(t);
+        return rc;
+    }
+    *out = t;
+    return GX_OK;
+}
+
+int gx_table_destroy(gx_table* t) {
+    if (!t) return GX_OK;
+    cudaStreamSynchronize(t->stream);
+    cudaFree(t->d.data);
+    cudaFree(t->d.status);
+    cudaFree(t->d_ctr);
+    cudaFreeHost(t->h_ctr);
+    t->keys.release();
+    t->codes.release();
+    t->handles.release();
+    t->aux.release();
+    t->aux2.release();
+    delete t;
+    return GX_OK;
+}
+
+int gx_table_clear(gx_table* t) {
+    const TableDesc& T = t->d;
+    GX_CUDA(cudaMemsetAsync(T.data, 0, T.nb * (uint64_t)T.bw * 4, t->stream));
+    GX_CUDA(cudaMemsetAsync(T.status, 0, T.nb * (uint64_t)T.stride, t->stream));
+    GX_CUDA(cudaMemsetAsync(t->d_ctr, 0, sizeof(uint64_t) * CTR_N, t->stream));
+    return GX_OK;
+}
+
+int gx_table_geometry(const gx_table* t, uint64_t* nb, int32_t* spb, uint64_t* ts) {
+    if (nb) *nb = t->d.nb;
+    if (spb) *spb = (int32_t)t->d.spb;
+    if (ts) *ts = t->total_slots;
+    return GX_OK;
+}
+
+int gx_table_hash_constants(const gx_table* t, uint64_t* a, uint64_t* b, uint64_t* salt) {
+    for (uint32_t i = 0; i < t->d.k; i++) {
+        if (a) a[i] = t->d.a[i];
+        if (b) b[i] = t->d.b[i];
+    }
+    if (salt) *salt = t->d.salt;
+    return GX_OK;
+}
+
+int gx_table_mode(const gx_table* t) { return (int)t->d.mode; }
+
+int gx_find_or_put(gx_table* t, const uint32_t* keys, uint64_t n, uint8_t* codes, int64_t* handles,
+                   int32_t serial) {
+    if (n == 0) return GX_OK;
+    const uint64_t v = t->d.vlen;
+    int rc = t->keys.ensure(sizeof(uint32_t) * n * v);
+    if (!rc) rc = t->codes.ensure(n);
+    if (!rc) rc = t->handles.ensure(sizeof(int64_t) * n);
+    if (rc) return rc;
+    GX_CUDA(cudaMemcpyAsync(t->keys.p, keys, sizeof(uint32_t) * n * v, cudaMemcpyHostToDevice,
+                            t->stream));
+    rc = table_find_or_put_dev(t, (const uint32_t*)t->keys.p, n, (uint8_t*)t->codes.p,
+                               (int64_t*)t->handles.p, serial, 0);
+    if (rc) return rc;
+    if (codes) GX_CUDA(cudaMemcpyAsync(codes, t->codes.p, n, cudaMemcpyDeviceToHost, t->stream));
+    if (handles)
+        GX_CUDA(cudaMemcpyAsync(handles, t->handles.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost,
+                                t->stream));
+    GX_CUDA(cudaStreamSynchronize(t->stream));
+    return GX_OK;
+}
+
+int gx_find_or_put_device(gx_table* t, const uint32_t* d_keys, uint64_t n, uint8_t* d_codes,
+                          int64_t* d_handles, uint64_t* inserted, uint64_t* full) {
+    unsigned long long before[CTR_N];
+    if (inserted || full) {
+        GX_CUDA(cudaMemcpyAsync(before, t->d_ctr, sizeof before, cudaMemcpyDeviceToHost, t->stream));
+    }
+    int rc = table_find_or_put_dev(t, d_keys, n, d_codes, d_handles, 0, 0);
+    if (rc) return rc;
+    if (inserted || full) {
+        GX_CUDA(cudaMemcpyAsync(t->h_ctr, t->d_ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost,
+                                t->stream));
+        GX_CUDA(cudaStreamSynchronize(t->stream));
+        if (inserted) *inserted = t->h_ctr[CTR_OCCUPIED] - before[CTR_OCCUPIED];
+        if (full) *full = t->h_ctr[CTR_FULL] - before[CTR_FULL];
+    }
+    return GX_OK;
+}
+
+int gx_claim_new(gx_table* t, const int64_t* handles, uint64_t n, uint8_t* claimed) {
+    if (n == 0) return GX_OK;
+    int rc = t->handles.ensure(sizeof(int64_t) * n);
+    if (!rc) rc = t->codes.ensure(n);
+    if (rc) return rc;
+    GX_CUDA(cudaMemcpyAsync(t->handles.p, handles, sizeof(int64_t) * n, cudaMemcpyHostToDevice,
+                            t->stream));
+    k_claim<<<(int)((n + 255) / 256), 256, 0, t->stream>>>(t->d, (const int64_t*)t->handles.p, n,
+                                                          (uint8_t*)t->codes.p,
+                                                          (unsigned long long*)t->d_ctr);
+    GX_LAUNCHED();
+    GX_CUDA(cudaMemcpyAsync(claimed, t->codes.p, n, cudaMemcpyDeviceToHost, t->stream));
+    GX_CUDA(cudaStreamSynchronize(t->stream));
+    return GX_OK;
+}
+
+int gx_scan_new(gx_table* t, uint64_t first, uint64_t last, int64_t* out, uint64_t cap,
+                uint64_t* count) {
+    return select_slots(t, first, last, SEL_NEW, out, nullptr, nullptr, out ? cap : 0, count);
+}
+
+int gx_occupancy(gx_table* t, uint64_t* occupied, uint64_t* new_count) {
+    GX_CUDA(cudaMemcpyAsync(t->h_ctr, t->d_ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost,
+                            t->stream));
+    GX_CUDA(cudaStreamSynchronize(t->stream));
+    if (occupied) *occupied = t->h_ctr[CTR_OCCUPIED];
+    if (new_count) *new_count = t->h_ctr[CTR_OCCUPIED] - t->h_ctr[CTR_OLD];
+    return GX_OK;
+}
+
+int gx_read_slots(gx_table* t, const int64_t* handles, uint64_t n, uint8_t* status, uint32_t* words) {
+    if (n == 0) return GX_OK;
+    const uint64_t v = t->d.vlen;
+    int rc = t->handles.ensure(sizeof(int64_t) * n);
+    if (!rc) rc = t->codes.ensure(n);
+    if (!rc) rc = t->keys.ensure(sizeof(uint32_t) * n * v);
+    if (rc) return rc;
+    GX_CUDA(cudaMemcpyAsync(t->handles.p, handles, sizeof(int64_t) * n, cudaMemcpyHostToDevice,
+                            t->stream));
+    k_read_slots<<<(int)((n + 255) / 256), 256, 0, t->stream>>>(
+        t->d, (const int64_t*)t->handles.p, n, (uint8_t*)t->codes.p, (uint32_t*)t->keys.p);
+    GX_LAUNCHED();
+    if (status) GX_CUDA(cudaMemcpyAsync(status, t->codes.p, n, cudaMemcpyDeviceToHost, t->stream));
+    if (words)
+        GX_CUDA(cudaMemcpyAsync(words, t->keys.p, sizeof(uint32_t) * n * v, cudaMemcpyDeviceToHost,
+                                t->stream));
+    GX_CUDA(cudaStreamSynchronize(t->stream));
+    return GX_OK;
+}
+
+int gx_dump(gx_table* t, int64_t* handles, uint8_t* status, uint32_t* words, uint64_t cap,
+            uint64_t* count) {
+    return select_slots(t, 0, t->d.nb, SEL_OCCUPIED, handles, status, words, cap, count);
+}
+
+}  // extern "C"
