@@ -1,0 +1,367 @@
+"""Benchmark driver (one JSON line on rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload ring16]
+  python bench.py --impl reference ...        # CPU reference arm
+
+Metric: states explored/sec of a full level-synchronous reachability run
+(BASELINE.json configs[3], the synthetically scaled token ring, rescaled
+to the chosen size).  A step = one complete exploration of the model from
+its initial state: table cleared, every BFS level expanded on the device,
+statuses finalised, report read back.
+
+  value      states / (device time of the K timed steps)  [inputs resident]
+  e2e        the same through the public API `explore(net, cfg)`: network
+             CSR uploaded from host memory, table allocated, report copied
+             back, every step
+  roofline   dominant kernel k_level: algorithmic bytes = transitions x
+             S(bw) + states x 12 vlen over the summed
+             CUDA-event time of its launches
+  cpu_baseline / --impl reference
+             the reference's bucket-partitioned parallel engine, ported to C
+             (oracle/gx_oracle.c, explore.py:212-351 restated), on the host
+             cores with all threads, on a bounded sample (token ring N=12)
+
+Between timed steps the table is re-zeroed (> L2 in size), so every step
+starts cold; inputs larger than L2 are stated in config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+TRAFFIC = ROOT / "profiles" / "traffic.json"
+METRIC = "states explored/sec"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--workload", default="ring16",
+                    help="ringN | gasN | petersonN (generated models)")
+    ap.add_argument("--bucket-words", type=int, default=32)
+    ap.add_argument("--hash-functions", type=int, default=8)
+    ap.add_argument("--load", type=float, default=0.5, help="target table load factor")
+    ap.add_argument("--probe-group", type=int, default=0)
+    ap.add_argument("--cpu-sample", default="ring12")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--hash-bench", action="store_true", help="add the bw x fill sweep")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+def model_path(name: str, root: Path) -> Path:
+    from paper_1801_05857_b200.bench import gen_gas_station, gen_peterson, gen_token_ring
+    kind = name.rstrip("0123456789")
+    n = int(name[len(kind):])
+    gen = {"ring": gen_token_ring, "gas": gen_gas_station, "peterson": gen_peterson}[kind]
+    return gen(n, root / name)[1]
+
+
+def closed_form(name: str):
+    """(states, transitions) known in closed form."""
+    if name.startswith("ring"):
+        n = int(name[4:])
+        return 2 * n * 3 ** (n - 1), 4 * n * n * 3 ** (n - 2)
+    return None
+
+
+def table_capacity(states_estimate: int, vlen: int, bw: int, load: float) -> int:
+    from paper_1801_05857_b200.hashtable import slots_per_bucket
+    layout = "half" if bw == 32 else "plain"
+    spb = slots_per_bucket(bw, vlen, layout)
+    buckets = int(states_estimate / load / spb) + 64
+    return buckets * bw
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_reference(sample: str, steps: int, warmup: int, tmp: Path):
+    """The reference engine's C port on all host threads, bounded sample."""
+    from oracle import oracle as O
+    path = model_path(sample, tmp)
+    net = O.Net.from_file(path)
+    threads = os.cpu_count() or 1
+    cf = closed_form(sample)
+    states_est = cf[0] if cf else 1 << 22
+    cap = table_capacity(states_est, net.vlen, 32, 0.5)
+    times, r = [], None
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        r = O.explore(net, capacity_words=cap, workers=threads)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    total = sum(times)
+    return {
+        "value": r.states * len(times) / total,
+        "unit": "states/s",
+        "cores": threads,
+        "kind": "port",
+        "sample": f"token ring N={sample[4:]} ({r.states} states, {r.transitions} transitions) "
+                  f"full exploration, {threads} worker threads, reference explore.py engine "
+                  f"restated in C (oracle/gx_oracle.c); {len(times)} timed runs",
+        "states": r.states,
+        "seconds_per_run": total / len(times),
+    }
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    with tempfile.TemporaryDirectory() as td:
+        base = cpu_reference(args.cpu_sample, args.steps, args.warmup, Path(td))
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": base["value"], "unit": "states/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * base["seconds_per_run"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (generated token-ring model)",
+        "config": {"workload": f"token ring N={args.cpu_sample[4:]} (bounded CPU sample of "
+                               f"configs[3])", "engine": "reference explore() port, C threads"},
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": base["value"], "unit": "states/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def hash_sweep(torch, peaks):
+    """Isolated FINDORPUT throughput vs bucket size and fill (configs[1])."""
+    from paper_1801_05857_b200.bench import device_insert_bench
+    from paper_1801_05857_b200.hashtable import StateTable, TableConfig
+    out = []
+    words = 1 << 31  # 8 GiB of slots: >> L2
+    for bw in (4, 8, 16, 32):
+        for k in (8, 32):
+            t = StateTable(TableConfig(bucket_words=bw, num_hash_functions=k, capacity_words=words),
+                           1, mark=(0, 31))
+            slots = t.total_slots
+            done = 0
+            for fill in (0.5, 0.6, 0.7, 0.8, 0.9):
+                target = int(fill * slots)
+                batch = int(0.02 * slots)
+                # untimed fill to (fill - 2%), then time the next 2% of inserts
+                if target - batch > done:
+                    r = device_insert_bench(t, target - batch - done, 1, seed=7, row_base=done)
+                    done += r["inserted"]
+                    if r["full"]:
+                        out.append({"bw": bw, "k": k, "fill": fill, "table_full": True})
+                        break
+                r = device_insert_bench(t, batch, 1, seed=7, row_base=done)
+                done += r["inserted"]
+                look = device_insert_bench(t, batch, 1, seed=7, row_base=done - batch)
+                cell = {"bw": bw, "k": k, "fill": fill, "insert_ops_per_sec": r["ops_per_sec"],
+                        "lookup_ops_per_sec": look["ops_per_sec"], "table_full": bool(r["full"])}
+                out.append(cell)
+                if r["full"]:
+                    break
+            t.close()
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_1801_05857_b200.distributed import bench_sharded
+        line = bench_sharded(args, torch, dist, model_path, closed_form, table_capacity)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        dist.destroy_process_group()
+        return
+
+    import paper_1801_05857_b200 as gx
+    from paper_1801_05857_b200 import _lib, statevec
+    from paper_1801_05857_b200.explore import ExploreConfig, Explorer
+    from paper_1801_05857_b200.hashtable import TableConfig
+
+    peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    tmp = Path(tempfile.mkdtemp())
+    path = model_path(args.workload, tmp)
+    net = gx.load_network(path)
+    scheme = statevec.make_scheme(net)
+    vlen = scheme.vector_length
+    cf = closed_form(args.workload)
+    states_est = cf[0] if cf else None
+    if states_est is None:
+        raise SystemExit("workload without a closed form needs --states")
+    cap = table_capacity(states_est, vlen, args.bucket_words, args.load)
+    tcfg = TableConfig(bucket_words=args.bucket_words, num_hash_functions=args.hash_functions,
+                       capacity_words=cap)
+    cfg = ExploreConfig(table=tcfg, detect_deadlocks=True, probe_group=args.probe_group)
+    stream = torch.cuda.current_stream().cuda_stream
+    ex = Explorer(net, cfg, stream=stream)
+    table_bytes = ex.table.num_buckets * (4 * args.bucket_words + ((ex.table.slots_per_bucket + 7) & ~7))
+
+    for _ in range(args.warmup):
+        rep = ex.run()
+    torch.cuda.synchronize()
+    launches0 = _lib.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(args.steps):
+            reps.append(ex.run())
+        ev1.record()
+        torch.cuda.synchronize()
+    launches = _lib.kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1)
+    rep = reps[-1]
+    if cf:
+        assert (rep.states, rep.transitions) == cf, (rep.states, rep.transitions, cf)
+    assert rep.outcome == "COMPLETE", rep.outcome
+    value = rep.states * args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (k_level), algorithmic bytes per step
+    s_bw = max(32, 4 * args.bucket_words)
+    alg_bytes = rep.transitions * s_bw + rep.states * 12 * vlen
+    level_ms = statistics.mean(r.level_ms for r in reps)
+    achieved = alg_bytes / (level_ms / 1e3) / 1e9
+    traffic = None
+    if TRAFFIC.exists():
+        tr = json.loads(TRAFFIC.read_text())
+        traffic = tr.get(f"{args.workload}/bw{args.bucket_words}")
+    ex.close()
+
+    # e2e through the public API with host buffers
+    torch.cuda.synchronize()
+    e2e_times = []
+    csr_bytes = None
+    for i in range(args.e2e_steps + 1):
+        t0 = time.perf_counter()
+        r = gx.explore(net, cfg)
+        dt = time.perf_counter() - t0
+        if i:
+            e2e_times.append(dt)
+    from paper_1801_05857_b200.explore import DeviceNetwork
+    dn = DeviceNetwork(net, scheme)
+    csr_bytes = dn.csr_bytes + 4 * vlen
+    dn.close()
+    e2e_value = r.states * len(e2e_times) / sum(e2e_times)
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0:
+        cpu = cpu_reference(args.cpu_sample, 2, 1, tmp)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "states/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (generated model, exact state space)",
+        "config": {
+            "workload": f"configs[3] scaled token ring N={args.workload[4:]}" if args.workload.startswith("ring")
+            else args.workload,
+            "states": rep.states, "transitions": rep.transitions, "levels": rep.iterations - 1,
+            "vector_words": vlen, "bucket_words": args.bucket_words,
+            "hash_functions": args.hash_functions, "table_bytes": table_bytes,
+            "load_factor": rep.states / ex.table.total_slots,
+            "l2_policy": "table re-zeroed every step; table >> 126 MB L2",
+            "parallelism": "single GPU",
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic,
+                     "kernel": "k_level", "algorithmic_bytes_per_step": alg_bytes,
+                     "kernel_ms_per_step": level_ms,
+                     "bytes_model": "transitions*max(32,4*bw) + states*12*vlen"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": csr_bytes,
+                "d2h_bytes_per_step": 64 + 400 * vlen,
+                "api": "paper_1801_05857_b200.explore(net, cfg) (allocates + frees the table)"},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "probes_per_step": rep.probes,
+    }
+    if args.hash_bench:
+        line["hash_bench"] = hash_sweep(torch, peaks)
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -180,6 +180,8 @@ typedef struct gx_report {
     uint64_t levels_launched;   /* expand kernels launched */
     uint64_t max_frontier;      /* widest BFS level */
     uint64_t kernels;           /* all kernels launched by this call */
+    double level_ms;            /* sum of the level kernels' CUDA-event durations */
+    uint64_t probes;            /* successors probed (FINDORPUT operations) */
 } gx_report;
 
 /* explore (explore.py:300-395): level-synchronous BFS from the network's

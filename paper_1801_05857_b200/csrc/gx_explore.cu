@@ -12,7 +12,7 @@
 namespace gx {
 
 // level counters live in the table's counter block
-enum { LV_NEW = 8, LV_TRANS = 9, LV_EXP = 10, LV_DL = 11, LV_FULL = 12, LV_OVF = 13 };
+enum { LV_NEW = 8, LV_TRANS = 9, LV_EXP = 10, LV_DL = 11, LV_FULL = 12, LV_OVF = 13, LV_PROBES = 14 };
 
 struct LevelArgs {
     const uint32_t* front;
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) k_level(TableDesc T, NetDesc N, LevelArgs
     uint32_t* q = qbuf[wid];
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-    unsigned long long trans = 0, expanded = 0;
+    unsigned long long trans = 0, expanded = 0, probes = 0;
     for (uint64_t base = warp * 32; base < A.nfront; base += nwarps * 32) {
         int stop = 0;
         if (lane == 0)
@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(256) k_level(TableDesc T, NetDesc N, LevelArgs
         }
         const uint32_t total = __shfl_sync(FULLMASK, incl, 31);
         const uint32_t excl = incl - n;
+        probes += total;
         for (uint32_t c0 = 0; c0 < total; c0 += QCAP) {
             const uint32_t c1 = min(total, c0 + (uint32_t)QCAP);
             if (has && n && excl < c1 && excl + n > c0) {
@@ -179,6 +180,7 @@ __global__ void __launch_bounds__(256) k_level(TableDesc T, NetDesc N, LevelArgs
     if (lane == 0) {
         if (trans) atomicAdd(&A.ctr[LV_TRANS], trans);
         if (expanded) atomicAdd(&A.ctr[LV_EXP], expanded);
+        if (probes) atomicAdd(&A.ctr[LV_PROBES], probes);
     }
 }
 
@@ -824,6 +826,9 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
         int rev = 1;
         unsigned long long new_base = 0, dl_base = 0;
         const int grid = persistent_grid();
+        cudaEvent_t la, lb;
+        GX_CUDA(cudaEventCreate(&la));
+        GX_CUDA(cudaEventCreate(&lb));
         for (;;) {
             const uint64_t claims = nF;
             max_front = std::max<uint64_t>(max_front, nF);
@@ -845,12 +850,19 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
                 A.dl_cap = dl_cap;
                 const uint64_t want = (nF + 31) / 32;  // warps
                 const int g = (int)std::min<uint64_t>((uint64_t)grid, (want + 7) / 8);
+                GX_CUDA(cudaEventRecord(la, st));
                 lk<<<g, 256, 0, st>>>(T, n->d, A);
                 GX_LAUNCHED();
+                GX_CUDA(cudaEventRecord(lb, st));
                 rep->levels_launched++;
             }
             GX_CUDA(cudaMemcpyAsync(hc, ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost, st));
             GX_CUDA(cudaStreamSynchronize(st));
+            if (claims) {
+                float lms = 0;
+                GX_CUDA(cudaEventElapsedTime(&lms, la, lb));
+                rep->level_ms += lms;
+            }
             nnew = hc[LV_NEW] - new_base;
             new_base = hc[LV_NEW];
             if (hc[LV_DL] > dl_base) {
@@ -887,6 +899,8 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
             nF = nnew;
             rev ^= 1;
         }
+        cudaEventDestroy(la);
+        cudaEventDestroy(lb);
     }
     GX_CUDA(cudaEventRecord(e1, st));
     // statuses as the reference leaves them: OLD except the unexpanded level
@@ -911,6 +925,7 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
     rep->deadlocks_kept = (int32_t)(kept.size() / v);
     if (deadlocks && !kept.empty()) memcpy(deadlocks, kept.data(), sizeof(uint32_t) * kept.size());
     rep->device_ms = ms;
+    rep->probes = hc[LV_PROBES];
     rep->max_frontier = max_front;
     rep->kernels = gx_kernel_launches() - launches0;
     return GX_OK;

@@ -1,0 +1,158 @@
+"""The hash-owner sharded driver (paper_1801_05857_b200/distributed.py) on
+CPU: world_size 2 over gloo, with the per-rank compute supplied by an
+oracle-backed stand-in (test infrastructure) instead of libgx.  Checks
+that routing, exchange, termination and the reductions reproduce the
+single-process results exactly."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT, golden_models, model_path
+
+MASK = (1 << 64) - 1
+
+
+def owner_of(h: int, ranks: int) -> int:
+    """Python restatement of gx_device.cuh owner_of (pinned against the
+    device in test_gpu_distributed.py)."""
+    z = h ^ 0x6A09E667F3BCC909
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK
+    z ^= z >> 31
+    return ((z >> 32) * ranks) >> 32
+
+
+class OracleShard:
+    """CPU stand-in for DeviceShard built on the oracle (tests only)."""
+
+    def __init__(self, path, table_kw, world, cap=1 << 16):
+        from oracle import oracle as O
+        from paper_1801_05857_b200 import load_network, statevec
+        self.O = O
+        self.net = O.Net.from_file(path)
+        self.scheme = statevec.make_scheme(load_network(path))
+        self.vlen = self.net.vlen
+        self.table_kw = table_kw
+        self.world = world
+        self.cap = cap
+        self.front = np.zeros((0, self.vlen), np.uint32)
+        z = lambda: torch.zeros((cap, self.vlen), dtype=torch.int32)
+        self.send, self.recv = z(), z()
+        self.salt = O.hash_constants(table_kw.get("seed", 42), 1)[1]
+        self._dl = []
+
+    def reset(self):
+        self.table = self.O.Table(vector_length=self.vlen, **self.table_kw)
+
+    def owner(self, packed):
+        arr = np.asarray(packed, np.uint32).reshape(-1, self.vlen)
+        return np.array([owner_of(self.O.fold(self.salt, r), self.world) for r in arr])
+
+    def seed_frontier(self, packed):
+        code, _ = self.table.find_or_insert(packed)
+        if code == 2:
+            return -1
+        self.front = packed.reshape(1, -1).astype(np.uint32)
+        return 1
+
+    def expand_route(self, nfront, detect):
+        succ, trans, dl = [], 0, 0
+        self._dl = []
+        for row in self.front[:nfront]:
+            s = self.net.unpack(row)
+            out, c = self.net.expand(s)
+            trans += c
+            if not out:
+                dl += 1
+                self._dl.append(row.copy())
+            succ += [self.net.pack(t) for _, t in out]
+        arr = np.array(succ, np.uint32).reshape(-1, self.vlen)
+        own = self.owner(arr) if len(arr) else np.zeros(0, np.int64)
+        order = np.argsort(own, kind="stable")
+        arr = arr[order]
+        counts = np.bincount(own, minlength=self.world)
+        self.send[: len(arr)] = torch.from_numpy(arr.astype(np.int32))
+        return torch.tensor(counts, dtype=torch.int64), trans, dl
+
+    def deadlock_vectors(self):
+        return np.array(self._dl, np.uint32).reshape(-1, self.vlen)
+
+    def insert_append(self, nrecv):
+        keys = self.recv[:nrecv].numpy().astype(np.uint32)
+        codes, _ = self.table.find_or_insert_batch(keys)
+        self.front = keys[codes == 1]
+        return int((codes == 1).sum()), bool((codes == 2).any())
+
+    def states(self):
+        return self.table.occupancy()[0]
+
+
+def _worker(rank, world, port, jobs, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1801_05857_b200.distributed import explore_sharded
+    from paper_1801_05857_b200 import statevec
+    out = []
+    for name, table_kw, max_it in jobs:
+        b = OracleShard(model_path(name), table_kw, world)
+        init = np.asarray(statevec.pack(b.scheme, b.net.initial), np.uint32)
+        r = explore_sharded(b, dist, torch, b.scheme, init, True, max_iterations=max_it)
+        out.append((name, r.states, r.transitions, r.iterations, r.deadlocks_total,
+                    tuple(map(tuple, r.deadlocks)), r.outcome, r.expanded))
+    if rank == 0:
+        q.put(out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def run_sharded(jobs, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, jobs, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+def test_sharded_matches_single_process():
+    from oracle import oracle as O
+    names = ["fig1", "ring6", "gas5", "phil4", "sinks8", "counter8", "sparse4", "collide", "rand3"]
+    jobs = [(n, {"capacity_words": 1 << 16}, None) for n in names]
+    res = run_sharded(jobs)
+    models = golden_models()
+    for (name, states, trans, iters, dl_total, dls, outcome, expanded) in res:
+        ref = O.explore(O.Net.from_file(model_path(name)), capacity_words=1 << 16,
+                        detect_deadlocks=True)
+        assert (states, trans, iters, dl_total, outcome, expanded) == \
+            (ref.states, ref.transitions, ref.iterations, ref.deadlocks_total, ref.outcome,
+             ref.expanded), name
+        b = models[name]["bfs"]
+        assert sorted(map(list, dls)) == sorted(b["deadlocks"])[:100], name
+
+
+def test_sharded_iteration_cap_and_table_full():
+    jobs = [("ring5", {"capacity_words": 1 << 14}, 3),
+            ("ring6", {"bucket_words": 4, "capacity_words": 4 * 64}, None)]
+    res = run_sharded(jobs)
+    from oracle import oracle as O
+    cap = O.explore(O.Net.from_file(model_path("ring5")), capacity_words=1 << 14, max_iterations=3)
+    name, states, trans, iters, _, _, outcome, _ = res[0]
+    assert (states, trans, iters, outcome) == (cap.states, cap.transitions, 3, "ITERATION_CAP")
+    name, states, _, _, _, _, outcome, _ = res[1]
+    assert outcome == "TABLE_FULL" and 0 < states < 2916
