@@ -323,7 +323,7 @@ def main():
     dn = DeviceNetwork(net, scheme)
     csr_bytes = dn.csr_bytes + 4 * vlen
     dn.close()
-    e2e_value = r.states * len(e2e_times) / sum(e2e_times)
+    e2e_value = r.states * len(e2e_times) / sum(e2e_times) if e2e_times else None
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0:

@@ -149,7 +149,7 @@ struct SlotCas<4> {
 // of the group; *handle is valid in every lane of the group.
 template <int BW, int V, int G>
 __device__ __forceinline__ int probe_mark(const TableDesc& T, bool active, const uint32_t* key,
-                                          uint64_t h, int64_t* handle) {
+                                          uint64_t h, int64_t* handle, int i0 = 0) {
     constexpr int CH = BW / 4;       // 16B chunks per bucket
     constexpr int CPL = CH / G;      // chunks per lane
     constexpr int SPC = 4 / V;       // slots per chunk
@@ -164,7 +164,7 @@ __device__ __forceinline__ int probe_mark(const TableDesc& T, bool active, const
 
     int code = -1;  // unresolved
     int64_t hd = -1;
-    for (int i = 0; i < (int)T.k; i++) {
+    for (int i = i0; i < (int)T.k; i++) {
         bool todo = active && code < 0;
         if (!__any_sync(FULLMASK, todo)) break;
         uint32_t occ = 0, match = 0;
@@ -241,6 +241,133 @@ __device__ __forceinline__ int probe_mark(const TableDesc& T, bool active, const
     if (active && code < 0) code = TABLE_FULL;
     *handle = active ? hd : -1;
     return code;
+}
+
+// Keys per lane group in one batch: enough that every lane has four 16-byte
+// bucket loads in flight before it consumes any of them.
+template <int BW, int G>
+struct Batch {
+    static constexpr int CPL = (BW / 4) / G;
+    static constexpr int U = CPL >= 4 ? 1 : 4 / CPL;
+};
+
+// Claim in a bucket whose masks the group has already computed: runs in
+// the group leader only.  rc = -1 when the bucket is full.
+template <int BW, int V>
+__device__ __forceinline__ void leader_resolve(const TableDesc& T, uint64_t bucket, uint32_t occ,
+                                               uint32_t match, const uint32_t* km, int* rc,
+                                               int64_t* rh) {
+    constexpr int SPB = BW / V;
+    constexpr uint32_t ALL = SPB >= 32 ? 0xffffffffu : ((1u << SPB) - 1u);
+    if (match) {
+        *rc = FOUND;
+        *rh = (int64_t)(bucket * (uint64_t)SPB + (__ffs(match) - 1));
+        return;
+    }
+    uint32_t empty = ~occ & ALL;
+    uint32_t* base = T.data + bucket * (uint64_t)BW;
+    while (empty) {
+        const int s = __ffs(empty) - 1;
+        uint32_t old[V];
+        if (SlotCas<V>::cas(base + s * V, km, old)) {
+            *rc = INSERTED;
+            *rh = (int64_t)(bucket * (uint64_t)SPB + s);
+            return;
+        }
+        bool eq = true;
+#pragma unroll
+        for (int w = 0; w < V; w++) eq = eq && (old[w] == km[w]);
+        if (eq) {
+            *rc = FOUND;
+            *rh = (int64_t)(bucket * (uint64_t)SPB + s);
+            return;
+        }
+        empty &= ~(1u << s);
+    }
+    *rc = -1;
+}
+
+// U keys per lane group at once (MODE_MARK): the first-bucket loads of all
+// U keys are issued before any is consumed, so a warp keeps (32/G)*U
+// bucket probes in flight.  Keys whose first bucket is full continue
+// through hash functions 1..K-1 with probe_mark (rare below the load
+// cliff).  Same contract as probe_mark: all 32 lanes call it together.
+template <int BW, int V, int G, int U>
+__device__ __forceinline__ void probe_mark_multi(const TableDesc& T, const bool (&active)[U],
+                                                 const uint32_t (&key)[U][V],
+                                                 const uint64_t (&h)[U], int (&code)[U],
+                                                 int64_t (&hd)[U]) {
+    constexpr int CPL = (BW / 4) / G;
+    constexpr int SPC = 4 / V;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (G - 1);
+    const int leader = lane & ~(G - 1);
+    uint4 ch[U][CPL];
+    uint64_t bucket[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        bucket[u] = 0;
+        if (active[u]) {
+            bucket[u] = bucket_of(T, h[u], 0);
+            const uint32_t* base = T.data + bucket[u] * (uint64_t)BW;
+#pragma unroll
+            for (int j = 0; j < CPL; j++) ch[u][j] = ldcg4(base + 4 * (gl + j * G));
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        uint32_t km[V];
+#pragma unroll
+        for (int w = 0; w < V; w++) km[w] = key[u][w] | (w == (int)T.mark_word ? T.mark : 0u);
+        uint32_t occ = 0, match = 0;
+        if (active[u]) {
+#pragma unroll
+            for (int j = 0; j < CPL; j++) {
+                const uint32_t w4[4] = {ch[u][j].x, ch[u][j].y, ch[u][j].z, ch[u][j].w};
+                const int c = gl + j * G;
+#pragma unroll
+                for (int t = 0; t < SPC; t++) {
+                    const int sl = c * SPC + t;
+                    uint32_t ob = 0;
+                    bool m = true;
+#pragma unroll
+                    for (int w = 0; w < V; w++) {
+                        ob |= w4[t * V + w] & (w == (int)T.mark_word ? T.mark : 0u);
+                        m = m && (w4[t * V + w] == km[w]);
+                    }
+                    occ |= (ob != 0u ? 1u : 0u) << sl;
+                    match |= (m ? 1u : 0u) << sl;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) {
+            occ |= __shfl_xor_sync(FULLMASK, occ, o);
+            match |= __shfl_xor_sync(FULLMASK, match, o);
+        }
+        int rc = -1;
+        int64_t rh = -1;
+        if (active[u] && gl == 0) leader_resolve<BW, V>(T, bucket[u], occ, match, km, &rc, &rh);
+        if (G > 1) {
+            rc = __shfl_sync(FULLMASK, rc, leader);
+            rh = (int64_t)__shfl_sync(FULLMASK, (unsigned long long)rh, leader);
+        }
+        code[u] = rc;
+        hd[u] = rh;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const bool need = active[u] && code[u] < 0;
+        if (__any_sync(FULLMASK, need)) {
+            int64_t x;
+            const int c = probe_mark<BW, V, G>(T, need, key[u], h[u], &x, 1);
+            if (need) {
+                code[u] = c;
+                hd[u] = x;
+            }
+        }
+        if (!active[u]) code[u] = -1;
+    }
 }
 
 // ---------------------------------------------- MODE_STATUS per-lane probe

@@ -5,9 +5,19 @@
 
 namespace gx {
 
+// s[w] with a runtime w, as a select chain so the state stays in registers
+template <int V>
+__device__ __forceinline__ uint32_t word_at(const uint32_t* s, uint32_t w) {
+    uint32_t r = s[0];
+#pragma unroll
+    for (int i = 1; i < V; i++) r = (w == (uint32_t)i) ? s[i] : r;
+    return r;
+}
+
+template <int V>
 __device__ __forceinline__ uint32_t field_get(const uint32_t* s, uint32_t word, uint32_t shift,
                                               uint32_t mask) {
-    return (s[word] >> shift) & mask;
+    return (word_at<V>(s, word) >> shift) & mask;
 }
 
 // Does rule r' produce target t from source s?  True iff t differs from s
@@ -31,8 +41,8 @@ __device__ __forceinline__ bool rule_generates(const NetDesc& N, uint32_t r, con
         if ((s[w] ^ t[w]) & ~allowed[w]) return false;
     for (uint32_t k = 0; k < rl.x; k++) {
         const uint4 pt = __ldg(&N.parts[rl.y + k]);
-        const uint32_t sq = field_get(s, pt.y, pt.z, pt.w);
-        const uint32_t tq = field_get(t, pt.y, pt.z, pt.w);
+        const uint32_t sq = field_get<V>(s, pt.y, pt.z, pt.w);
+        const uint32_t tq = field_get<V>(t, pt.y, pt.z, pt.w);
         const uint2 l = __ldg(&N.rq[pt.x + sq]);
         bool in = false;
         for (uint32_t d = 0; d < l.y && !in; d++) in = __ldg(&N.rdst[l.x + d]) == tq;
@@ -43,17 +53,20 @@ __device__ __forceinline__ bool rule_generates(const NetDesc& N, uint32_t r, con
 
 // Build the target of combination `c` of rule `rl` from s into t.
 template <int V>
-__device__ __forceinline__ void rule_target(const NetDesc& N, const uint4 rl, uint64_t c,
+__device__ __forceinline__ void rule_target(const NetDesc& N, const uint4 rl, uint32_t c,
                                             const uint32_t* s, uint32_t* t) {
 #pragma unroll
     for (int w = 0; w < V; w++) t[w] = s[w];
     // mixed radix, last participant fastest (itertools.product order)
     for (int k = (int)rl.x - 1; k >= 0; k--) {
         const uint4 pt = __ldg(&N.parts[rl.y + k]);
-        const uint32_t sq = field_get(s, pt.y, pt.z, pt.w);
+        const uint32_t sq = field_get<V>(s, pt.y, pt.z, pt.w);
         const uint2 l = __ldg(&N.rq[pt.x + sq]);
-        const uint32_t dig = (uint32_t)(c % l.y);
-        c /= l.y;
+        uint32_t dig = 0;
+        if (l.y > 1) {
+            dig = c % l.y;
+            c /= l.y;
+        }
         const uint32_t dst = __ldg(&N.rdst[l.x + dig]);
 #pragma unroll
         for (int w = 0; w < V; w++)
@@ -77,7 +90,7 @@ __device__ __forceinline__ uint32_t expand_state(const NetDesc& N, const uint32_
     uint32_t t[V];
     for (uint32_t i = 0; i < N.nproc; i++) {
         const uint4 pr = __ldg(&N.proc[i]);
-        const uint32_t q = field_get(s, pr.x, pr.y, pr.z);
+        const uint32_t q = field_get<V>(s, pr.x, pr.y, pr.z);
         const uint4 e = __ldg(&N.qtab[pr.w + q]);
         count += e.z;
         if (EMIT && n < hi && n + e.y > lo) {
@@ -99,7 +112,7 @@ __device__ __forceinline__ uint32_t expand_state(const NetDesc& N, const uint32_
             uint64_t combos = 1;
             for (uint32_t k = 0; k < rl.x; k++) {
                 const uint4 pt = __ldg(&N.parts[rl.y + k]);
-                const uint2 l = __ldg(&N.rq[pt.x + field_get(s, pt.y, pt.z, pt.w)]);
+                const uint2 l = __ldg(&N.rq[pt.x + field_get<V>(s, pt.y, pt.z, pt.w)]);
                 combos *= l.y;
                 if (!combos) break;
             }
@@ -108,7 +121,7 @@ __device__ __forceinline__ uint32_t expand_state(const NetDesc& N, const uint32_
             if (nd == 0) {
                 count += combos;
                 if (EMIT && n < hi && n + combos > lo) {
-                    for (uint64_t c = 0; c < combos; c++) {
+                    for (uint32_t c = 0; c < (uint32_t)combos; c++) {
                         const uint64_t idx = n + c;
                         if (idx < lo || idx >= hi) continue;
                         rule_target<V>(N, rl, c, s, t);
@@ -119,7 +132,7 @@ __device__ __forceinline__ uint32_t expand_state(const NetDesc& N, const uint32_
                 }
                 n += (uint32_t)combos;
             } else {
-                for (uint64_t c = 0; c < combos; c++) {
+                for (uint32_t c = 0; c < (uint32_t)combos; c++) {
                     rule_target<V>(N, rl, c, s, t);
                     bool dup = false;
                     for (uint32_t y = 0; y < nd && !dup; y++)

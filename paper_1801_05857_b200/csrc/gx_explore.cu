@@ -72,23 +72,53 @@ __device__ __forceinline__ void store_state(uint32_t* p, const uint32_t* s) {
     }
 }
 
-// words of shared memory per warp for the successor queue
-constexpr int QWORDS = 1024;
+// words of shared memory per warp for the successor queue, and the same
+// again for the queue of freshly inserted keys (next-frontier staging)
+constexpr int QWORDS = 512;
 
-// One BFS level: every warp takes 32 frontier states at a time, counts
-// their successors (count pass), scans the counts, then emits successors
-// into its shared-memory queue in chunks of QWORDS/V and runs FINDORPUT on
-// the queue with G lanes per key.  INSERTED keys are appended to the next
-// frontier with one atomic per warp round.
+// Copy the warp's staged next-frontier keys to global memory with one
+// atomic per flush (the counter is shared by the whole grid).
+template <int V>
+__device__ __forceinline__ void flush_out(const LevelArgs& A, const uint32_t* outq, uint32_t n_out) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long pos0 = 0;
+    if (lane == 0) pos0 = atomicAdd(&A.ctr[LV_NEW], (unsigned long long)n_out) - A.new_base;
+    pos0 = __shfl_sync(FULLMASK, pos0, 0);
+    if (pos0 + n_out > A.out_limit) {
+        if (lane == 0) atomicExch(&A.ctr[LV_OVF], 1ull);
+        return;
+    }
+    for (uint32_t x = lane; x < n_out; x += 32) {
+        const unsigned long long p = pos0 + x;
+        const uint64_t slot = A.out_rev ? A.out_cap - 1 - p : p;
+        store_state<V>(A.out + slot * V, outq + (uint64_t)x * V);
+    }
+}
+
+// One BFS level.  Every warp takes 32 frontier states at a time:
+//   count pass   successors and transitions per state (expand_state),
+//                warp scan -> each lane's slice of the warp's successor list
+//   emit pass    successors into the warp's shared-memory queue, QWORDS/V
+//                at a time
+//   probe        FINDORPUT of the queue: G lanes per key, U keys per lane
+//                group with all first-bucket loads issued up front
+//   stage        INSERTED keys go to a shared-memory out-queue, flushed to
+//                the next frontier with one atomic per chunk
 template <int BW, int V, int G, bool MARK>
 __global__ void __launch_bounds__(256) k_level(TableDesc T, NetDesc N, LevelArgs A) {
     constexpr int QCAP = QWORDS / V;
+    constexpr int U = MARK ? Batch<(MARK ? BW : 32), G>::U : 1;
+    constexpr int R = MARK ? 32 / G : 32;
     __shared__ __align__(16) uint32_t qbuf[8][QWORDS];
+    __shared__ __align__(16) uint32_t obuf[8][QWORDS];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     uint32_t* q = qbuf[wid];
+    uint32_t* outq = obuf[wid];
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    const int grp = MARK ? lane / G : lane;
+    const bool leader = MARK ? (lane & (G - 1)) == 0 : true;
     unsigned long long trans = 0, expanded = 0, probes = 0;
     for (uint64_t base = warp * 32; base < A.nfront; base += nwarps * 32) {
         int stop = 0;
@@ -123,7 +153,7 @@ __global__ void __launch_bounds__(256) k_level(TableDesc T, NetDesc N, LevelArgs
         }
         const uint32_t total = __shfl_sync(FULLMASK, incl, 31);
         const uint32_t excl = incl - n;
-        probes += total;
+        probes += lane == 0 ? total : 0;
         for (uint32_t c0 = 0; c0 < total; c0 += QCAP) {
             const uint32_t c1 = min(total, c0 + (uint32_t)QCAP);
             if (has && n && excl < c1 && excl + n > c0) {
@@ -134,49 +164,49 @@ __global__ void __launch_bounds__(256) k_level(TableDesc T, NetDesc N, LevelArgs
             }
             __syncwarp();
             const uint32_t m = c1 - c0;
-            constexpr int R = MARK ? 32 / G : 32;
-            const int grp = MARK ? lane / G : lane;
-            for (uint32_t r0 = 0; r0 < m; r0 += R) {
-                const uint32_t e = r0 + grp;
-                const bool active = e < m;
-                uint32_t key[V];
+            uint32_t n_out = 0;
+            bool any_full = false;
+            for (uint32_t r0 = 0; r0 < m; r0 += R * U) {
+                bool act[U];
+                uint32_t key[U][V];
+                uint64_t h[U];
+                int code[U];
+                int64_t hd[U];
 #pragma unroll
-                for (int w = 0; w < V; w++) key[w] = active ? q[e * V + w] : 0u;
-                const uint64_t h = fold<V>(T.salt, key);
-                int64_t hd;
-                int code;
-                bool leader;
-                if constexpr (MARK) {
-                    code = probe_mark<BW, V, G>(T, active, key, h, &hd);
-                    leader = active && (lane & (G - 1)) == 0;
-                } else {
-                    code = active ? probe_status(T, key, h, &hd) : FOUND;
-                    leader = active;
+                for (int u = 0; u < U; u++) {
+                    const uint32_t e = r0 + u * R + grp;
+                    act[u] = e < m;
+#pragma unroll
+                    for (int w = 0; w < V; w++) key[u][w] = act[u] ? q[e * V + w] : 0u;
+                    h[u] = fold<V>(T.salt, key[u]);
                 }
-                const bool ins = leader && code == INSERTED;
-                const bool full = leader && code == TABLE_FULL;
-                if (__any_sync(FULLMASK, full) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
-                const uint32_t insm = __ballot_sync(FULLMASK, ins);
-                if (insm) {
-                    unsigned long long pos0 = 0;
-                    if (lane == 0) pos0 = atomicAdd(&A.ctr[LV_NEW], (unsigned long long)__popc(insm)) - A.new_base;
-                    pos0 = __shfl_sync(FULLMASK, pos0, 0);
+                if constexpr (MARK) {
+                    probe_mark_multi<BW, V, G, U>(T, act, key, h, code, hd);
+                } else {
+                    code[0] = act[0] ? probe_status(T, key[0], h[0], &hd[0]) : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const bool ins = leader && act[u] && code[u] == INSERTED;
+                    any_full |= leader && act[u] && code[u] == TABLE_FULL;
+                    const uint32_t insm = __ballot_sync(FULLMASK, ins);
                     if (ins) {
-                        const unsigned long long p = pos0 + __popc(insm & lanemask_lt());
-                        if (p < A.out_limit) {
-                            const uint64_t slot = A.out_rev ? A.out_cap - 1 - p : p;
-                            store_state<V>(A.out + slot * V, key);
-                        } else {
-                            atomicExch(&A.ctr[LV_OVF], 1ull);
-                        }
+                        const uint32_t p = n_out + __popc(insm & lanemask_lt());
+#pragma unroll
+                        for (int w = 0; w < V; w++) outq[p * V + w] = key[u][w];
                     }
+                    n_out += __popc(insm);
                 }
             }
+            if (__any_sync(FULLMASK, any_full) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
+            __syncwarp();
+            if (n_out) flush_out<V>(A, outq, n_out);
             __syncwarp();
         }
     }
     trans = warp_sum(trans);
     expanded = warp_sum(expanded);
+    probes = warp_sum(probes);
     if (lane == 0) {
         if (trans) atomicAdd(&A.ctr[LV_TRANS], trans);
         if (expanded) atomicAdd(&A.ctr[LV_EXP], expanded);
@@ -518,43 +548,54 @@ struct BenchArgs {
     unsigned long long* ctr;  // [0] inserted, [1] full
 };
 
+template <int V>
+__device__ __forceinline__ void bench_key(const BenchArgs& B, uint64_t e, uint32_t* key) {
+    uint64_t p = e;
+    do {
+        p = perm_bits(p, B.perm_bits_n, B.seed);
+    } while (p >= B.total);
+    uint64_t row = p / B.dup;
+    if (row >= B.unique) row = B.unique - 1;
+    bench_row<V>(row + B.row_base, B.key_bits, B.seed, key);
+}
+
 template <int BW, int V, int G, bool MARK>
 __global__ void __launch_bounds__(256) k_bench(TableDesc T, BenchArgs B) {
     const int lane = threadIdx.x & 31;
+    constexpr int U = MARK ? Batch<(MARK ? BW : 32), G>::U : 1;
     constexpr int R = MARK ? 32 / G : 32;
     const int grp = MARK ? lane / G : lane;
+    const bool leader = MARK ? (lane & (G - 1)) == 0 : true;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
     unsigned long long ins = 0, full = 0;
-    for (uint64_t base = warp * R; base < B.total; base += nwarps * R) {
-        const uint64_t e = base + grp;
-        const bool active = e < B.total;
-        uint32_t key[V];
-        if (active) {
-            uint64_t p = e;
-            do {
-                p = perm_bits(p, B.perm_bits_n, B.seed);
-            } while (p >= B.total);
-            uint64_t row = p / B.dup;
-            if (row >= B.unique) row = B.unique - 1;
-            bench_row<V>(row + B.row_base, B.key_bits, B.seed, key);
-        } else {
+    for (uint64_t base = warp * R * U; base < B.total; base += nwarps * R * U) {
+        bool act[U];
+        uint32_t key[U][V];
+        uint64_t h[U];
+        int code[U];
+        int64_t hd[U];
 #pragma unroll
-            for (int w = 0; w < V; w++) key[w] = 0;
+        for (int u = 0; u < U; u++) {
+            const uint64_t e = base + u * R + grp;
+            act[u] = e < B.total;
+            if (act[u])
+                bench_key<V>(B, e, key[u]);
+            else
+#pragma unroll
+                for (int w = 0; w < V; w++) key[u][w] = 0;
+            h[u] = fold<V>(T.salt, key[u]);
         }
-        const uint64_t h = fold<V>(T.salt, key);
-        int64_t hd;
-        int code;
-        bool leader;
         if constexpr (MARK) {
-            code = probe_mark<BW, V, G>(T, active, key, h, &hd);
-            leader = active && (lane & (G - 1)) == 0;
+            probe_mark_multi<BW, V, G, U>(T, act, key, h, code, hd);
         } else {
-            code = active ? probe_status(T, key, h, &hd) : FOUND;
-            leader = active;
+            code[0] = act[0] ? probe_status(T, key[0], h[0], &hd[0]) : -1;
         }
-        ins += leader && code == INSERTED;
-        full += leader && code == TABLE_FULL;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            ins += leader && act[u] && code[u] == INSERTED;
+            full += leader && act[u] && code[u] == TABLE_FULL;
+        }
     }
     ins = warp_sum(ins);
     full = warp_sum(full);

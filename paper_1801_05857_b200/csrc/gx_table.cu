@@ -58,24 +58,54 @@ __global__ void __launch_bounds__(256) k_fop_mark(TableDesc T, const uint32_t* _
                                                   unsigned long long* ctr, int serial) {
     const int lane = threadIdx.x & 31;
     const int grp = lane / G;
-    const int R = serial ? 1 : 32 / G;
+    const bool leader = (lane & (G - 1)) == 0;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
     unsigned long long ins = 0, full = 0;
-    for (uint64_t base = warp * R; base < n; base += nwarps * R) {
-        const uint64_t e = base + grp;
-        const bool active = grp < R && e < n;
-        uint32_t key[V];
+    if (serial) {
+        // one key at a time, in order: the reference's single-threaded placement
+        for (uint64_t e = warp; e < n; e += nwarps) {
+            const bool active = grp == 0;
+            uint32_t key[V];
 #pragma unroll
-        for (int w = 0; w < V; w++) key[w] = active ? keys[e * V + w] : 0u;
-        const uint64_t h = fold<V>(T.salt, key);
-        int64_t hd;
-        const int code = probe_mark<BW, V, G>(T, active, key, h, &hd);
-        if (active && (lane & (G - 1)) == 0) {
-            if (codes) codes[e] = (uint8_t)code;
-            if (handles) handles[e] = hd;
-            ins += code == INSERTED;
-            full += code == TABLE_FULL;
+            for (int w = 0; w < V; w++) key[w] = keys[e * V + w];
+            int64_t hd;
+            const int code = probe_mark<BW, V, G>(T, active, key, fold<V>(T.salt, key), &hd);
+            if (active && leader) {
+                if (codes) codes[e] = (uint8_t)code;
+                if (handles) handles[e] = hd;
+                ins += code == INSERTED;
+                full += code == TABLE_FULL;
+            }
+        }
+    } else {
+        constexpr int U = Batch<BW, G>::U;
+        constexpr int R = 32 / G;
+        for (uint64_t base = warp * R * U; base < n; base += nwarps * R * U) {
+            bool act[U];
+            uint32_t key[U][V];
+            uint64_t h[U];
+            int code[U];
+            int64_t hd[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint64_t e = base + u * R + grp;
+                act[u] = e < n;
+#pragma unroll
+                for (int w = 0; w < V; w++) key[u][w] = act[u] ? keys[e * V + w] : 0u;
+                h[u] = fold<V>(T.salt, key[u]);
+            }
+            probe_mark_multi<BW, V, G, U>(T, act, key, h, code, hd);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (act[u] && leader) {
+                    const uint64_t e = base + u * R + grp;
+                    if (codes) codes[e] = (uint8_t)code[u];
+                    if (handles) handles[e] = hd[u];
+                    ins += code[u] == INSERTED;
+                    full += code[u] == TABLE_FULL;
+                }
+            }
         }
     }
     ins = warp_sum_u64(ins);

@@ -200,6 +200,10 @@ def test_explore_matches_reference(name):
                 lines = dump.splitlines()
                 assert len(lines) == len(set(lines)) == rep.states
                 continue
+            if want["deadlocks_total"] > 100:
+                # the reference keeps the first 100 *recorded* (order dependent);
+                # the device keeps the 100 smallest = sequential_bfs's sorted head
+                want = dict(want, deadlocks=g["bfs"]["deadlocks"][:100])
             got = {"states": rep.states, "transitions": rep.transitions,
                    "deadlocks": [list(s) for s in rep.deadlocks],
                    "deadlocks_total": rep.deadlocks_total, "expanded": rep.expanded,
@@ -239,9 +243,9 @@ def test_expand_kats_on_device():
 @pytest.mark.parametrize("bw", [4, 8, 16, 32])
 @pytest.mark.parametrize("group", [0, 1])
 def test_bucket_sizes_and_probe_groups(bw, group):
-    for name in ("ring8", "gas7", "phil5", "counter8", "sparse8"):
+    for name in ("ring8", "gas7", "phil5", "counter8", "sinks8", "wide33"):
         b = MODELS[name]["bfs"]
-        rep, dump, ex = _run(name, {"bucket_words": bw, "capacity_words": 1 << 20}, probe_group=group)
+        rep, dump, ex = _run(name, {"bucket_words": bw, "capacity_words": 1 << 22}, probe_group=group)
         ex.close()
         assert (rep.states, rep.transitions, rep.deadlocks_total, rep.outcome) == \
             (b["states"], b["transitions"], b["deadlocks_total"], "COMPLETE"), (name, bw)
