@@ -243,14 +243,6 @@ __device__ __forceinline__ int probe_mark(const TableDesc& T, bool active, const
     return code;
 }
 
-// Keys per lane group in one batch: enough that every lane has four 16-byte
-// bucket loads in flight before it consumes any of them.
-template <int BW, int G>
-struct Batch {
-    static constexpr int CPL = (BW / 4) / G;
-    static constexpr int U = CPL >= 4 ? 1 : 4 / CPL;
-};
-
 // Claim in a bucket whose masks the group has already computed: runs in
 // the group leader only.  rc = -1 when the bucket is full.
 template <int BW, int V>
@@ -287,28 +279,56 @@ __device__ __forceinline__ void leader_resolve(const TableDesc& T, uint64_t buck
     *rc = -1;
 }
 
-// U keys per lane group at once (MODE_MARK): the first-bucket loads of all
-// U keys are issued before any is consumed, so a warp keeps (32/G)*U
-// bucket probes in flight.  Keys whose first bucket is full continue
-// through hash functions 1..K-1 with probe_mark (rare below the load
-// cliff).  Same contract as probe_mark: all 32 lanes call it together.
-template <int BW, int V, int G, int U>
-__device__ __forceinline__ void probe_mark_multi(const TableDesc& T, const bool (&active)[U],
-                                                 const uint32_t (&key)[U][V],
-                                                 const uint64_t (&h)[U], int (&code)[U],
-                                                 int64_t (&hd)[U]) {
-    constexpr int CPL = (BW / 4) / G;
+// ----------------------------------------------------- batched probing
+//
+// A warp probes KB = 32*M keys per batch.  Lane l owns keys l + 32*m
+// (m < M): it computes their fold and first bucket once.  Lane group grp
+// (G lanes) then handles keys e = u*R + grp for u < U = M*G (R = 32/G
+// groups), pulling each key's words and bucket from its owner lane
+// ((u % G)*R + grp, slot u / G -- both compile-time in u) by shuffle, and
+// issues all U*CPL 16-byte bucket loads before consuming any.  The group
+// leader resolves each key (FOUND / CAS-insert / bucket full); keys whose
+// first bucket is full continue through hash functions 1..K-1 with
+// probe_mark (rare below the load cliff).
+template <int BW, int G>
+struct ProbeShape {
+    static constexpr int CH = BW / 4;     // 16-byte chunks per bucket
+    static constexpr int CPL = CH / G;    // chunks per lane per key
+    static constexpr int M = BW >= 32 ? 1 : (4 / CH > 1 ? 4 / CH : 1);  // owned keys per lane
+    static constexpr int U = M * G;       // keys per lane group per batch
+    static constexpr int R = 32 / G;      // lane groups per warp
+    static constexpr int KB = 32 * M;     // keys per warp per batch
+};
+
+template <int BW, int V, int G>
+__device__ __forceinline__ void probe_batch(const TableDesc& T,
+                                            const uint32_t (&own_key)[ProbeShape<BW, G>::M][V],
+                                            const bool (&own_act)[ProbeShape<BW, G>::M],
+                                            uint32_t (&key)[ProbeShape<BW, G>::U][V],
+                                            bool (&act)[ProbeShape<BW, G>::U],
+                                            int (&code)[ProbeShape<BW, G>::U],
+                                            int64_t (&hd)[ProbeShape<BW, G>::U]) {
+    using S = ProbeShape<BW, G>;
+    constexpr int M = S::M, U = S::U, R = S::R, CPL = S::CPL;
     constexpr int SPC = 4 / V;
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
+    const int grp = lane / G;
     const int leader = lane & ~(G - 1);
+    uint64_t own_b[M];
+#pragma unroll
+    for (int m = 0; m < M; m++) own_b[m] = own_act[m] ? bucket_of(T, fold<V>(T.salt, own_key[m]), 0) : 0;
     uint4 ch[U][CPL];
     uint64_t bucket[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-        bucket[u] = 0;
-        if (active[u]) {
-            bucket[u] = bucket_of(T, h[u], 0);
+        const int src = (u % G) * R + grp;
+        const int m = u / G;
+        act[u] = __shfl_sync(FULLMASK, own_act[m] ? 1 : 0, src) != 0;
+        bucket[u] = __shfl_sync(FULLMASK, (unsigned long long)own_b[m], src);
+#pragma unroll
+        for (int w = 0; w < V; w++) key[u][w] = __shfl_sync(FULLMASK, own_key[m][w], src);
+        if (act[u]) {
             const uint32_t* base = T.data + bucket[u] * (uint64_t)BW;
 #pragma unroll
             for (int j = 0; j < CPL; j++) ch[u][j] = ldcg4(base + 4 * (gl + j * G));
@@ -320,7 +340,7 @@ __device__ __forceinline__ void probe_mark_multi(const TableDesc& T, const bool 
 #pragma unroll
         for (int w = 0; w < V; w++) km[w] = key[u][w] | (w == (int)T.mark_word ? T.mark : 0u);
         uint32_t occ = 0, match = 0;
-        if (active[u]) {
+        if (act[u]) {
 #pragma unroll
             for (int j = 0; j < CPL; j++) {
                 const uint32_t w4[4] = {ch[u][j].x, ch[u][j].y, ch[u][j].z, ch[u][j].w};
@@ -329,14 +349,14 @@ __device__ __forceinline__ void probe_mark_multi(const TableDesc& T, const bool 
                 for (int t = 0; t < SPC; t++) {
                     const int sl = c * SPC + t;
                     uint32_t ob = 0;
-                    bool m = true;
+                    bool mm = true;
 #pragma unroll
                     for (int w = 0; w < V; w++) {
                         ob |= w4[t * V + w] & (w == (int)T.mark_word ? T.mark : 0u);
-                        m = m && (w4[t * V + w] == km[w]);
+                        mm = mm && (w4[t * V + w] == km[w]);
                     }
                     occ |= (ob != 0u ? 1u : 0u) << sl;
-                    match |= (m ? 1u : 0u) << sl;
+                    match |= (mm ? 1u : 0u) << sl;
                 }
             }
         }
@@ -347,26 +367,22 @@ __device__ __forceinline__ void probe_mark_multi(const TableDesc& T, const bool 
         }
         int rc = -1;
         int64_t rh = -1;
-        if (active[u] && gl == 0) leader_resolve<BW, V>(T, bucket[u], occ, match, km, &rc, &rh);
-        if (G > 1) {
-            rc = __shfl_sync(FULLMASK, rc, leader);
-            rh = (int64_t)__shfl_sync(FULLMASK, (unsigned long long)rh, leader);
-        }
-        code[u] = rc;
+        if (act[u] && gl == 0) leader_resolve<BW, V>(T, bucket[u], occ, match, km, &rc, &rh);
+        if (G > 1) rc = __shfl_sync(FULLMASK, rc, leader);
+        code[u] = act[u] ? rc : -1;
         hd[u] = rh;
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
-        const bool need = active[u] && code[u] < 0;
+        const bool need = act[u] && code[u] < 0;
         if (__any_sync(FULLMASK, need)) {
             int64_t x;
-            const int c = probe_mark<BW, V, G>(T, need, key[u], h[u], &x, 1);
+            const int c = probe_mark<BW, V, G>(T, need, key[u], fold<V>(T.salt, key[u]), &x, 1);
             if (need) {
                 code[u] = c;
                 hd[u] = x;
             }
         }
-        if (!active[u]) code[u] = -1;
     }
 }
 

@@ -104,11 +104,13 @@ __device__ __forceinline__ void flush_out(const LevelArgs& A, const uint32_t* ou
 //                group with all first-bucket loads issued up front
 //   stage        INSERTED keys go to a shared-memory out-queue, flushed to
 //                the next frontier with one atomic per chunk
+#ifndef GX_LEVEL_MINB
+#define GX_LEVEL_MINB 2  // resident blocks per SM the level kernel is compiled for
+#endif
+
 template <int BW, int V, int G, bool MARK>
-__global__ void __launch_bounds__(256) k_level(TableDesc T, NetDesc N, LevelArgs A) {
+__global__ void __launch_bounds__(256, GX_LEVEL_MINB) k_level(TableDesc T, NetDesc N, LevelArgs A) {
     constexpr int QCAP = QWORDS / V;
-    constexpr int U = MARK ? Batch<(MARK ? BW : 32), G>::U : 1;
-    constexpr int R = MARK ? 32 / G : 32;
     __shared__ __align__(16) uint32_t qbuf[8][QWORDS];
     __shared__ __align__(16) uint32_t obuf[8][QWORDS];
     const int lane = threadIdx.x & 31;
@@ -117,7 +119,6 @@ __global__ void __launch_bounds__(256) k_level(TableDesc T, NetDesc N, LevelArgs
     uint32_t* outq = obuf[wid];
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-    const int grp = MARK ? lane / G : lane;
     const bool leader = MARK ? (lane & (G - 1)) == 0 : true;
     unsigned long long trans = 0, expanded = 0, probes = 0;
     for (uint64_t base = warp * 32; base < A.nfront; base += nwarps * 32) {
@@ -166,34 +167,52 @@ __global__ void __launch_bounds__(256) k_level(TableDesc T, NetDesc N, LevelArgs
             const uint32_t m = c1 - c0;
             uint32_t n_out = 0;
             bool any_full = false;
-            for (uint32_t r0 = 0; r0 < m; r0 += R * U) {
-                bool act[U];
-                uint32_t key[U][V];
-                uint64_t h[U];
-                int code[U];
-                int64_t hd[U];
+            if constexpr (MARK) {
+                using S = ProbeShape<BW, G>;
+                for (uint32_t r0 = 0; r0 < m; r0 += S::KB) {
+                    uint32_t own_key[S::M][V];
+                    bool own_act[S::M];
 #pragma unroll
-                for (int u = 0; u < U; u++) {
-                    const uint32_t e = r0 + u * R + grp;
-                    act[u] = e < m;
+                    for (int mm = 0; mm < S::M; mm++) {
+                        const uint32_t e = r0 + lane + 32 * mm;
+                        own_act[mm] = e < m;
 #pragma unroll
-                    for (int w = 0; w < V; w++) key[u][w] = act[u] ? q[e * V + w] : 0u;
-                    h[u] = fold<V>(T.salt, key[u]);
+                        for (int w = 0; w < V; w++) own_key[mm][w] = own_act[mm] ? q[e * V + w] : 0u;
+                    }
+                    uint32_t key[S::U][V];
+                    bool act[S::U];
+                    int code[S::U];
+                    int64_t hd[S::U];
+                    probe_batch<BW, V, G>(T, own_key, own_act, key, act, code, hd);
+#pragma unroll
+                    for (int u = 0; u < S::U; u++) {
+                        const bool ins = leader && act[u] && code[u] == INSERTED;
+                        any_full |= leader && act[u] && code[u] == TABLE_FULL;
+                        const uint32_t insm = __ballot_sync(FULLMASK, ins);
+                        if (ins) {
+                            const uint32_t p = n_out + __popc(insm & lanemask_lt());
+#pragma unroll
+                            for (int w = 0; w < V; w++) outq[p * V + w] = key[u][w];
+                        }
+                        n_out += __popc(insm);
+                    }
                 }
-                if constexpr (MARK) {
-                    probe_mark_multi<BW, V, G, U>(T, act, key, h, code, hd);
-                } else {
-                    code[0] = act[0] ? probe_status(T, key[0], h[0], &hd[0]) : -1;
-                }
+            } else {
+                for (uint32_t r0 = 0; r0 < m; r0 += 32) {
+                    const uint32_t e = r0 + lane;
+                    const bool act = e < m;
+                    uint32_t key[V];
 #pragma unroll
-                for (int u = 0; u < U; u++) {
-                    const bool ins = leader && act[u] && code[u] == INSERTED;
-                    any_full |= leader && act[u] && code[u] == TABLE_FULL;
+                    for (int w = 0; w < V; w++) key[w] = act ? q[e * V + w] : 0u;
+                    int64_t hd;
+                    const int code = act ? probe_status(T, key, fold<V>(T.salt, key), &hd) : -1;
+                    const bool ins = act && code == INSERTED;
+                    any_full |= act && code == TABLE_FULL;
                     const uint32_t insm = __ballot_sync(FULLMASK, ins);
                     if (ins) {
                         const uint32_t p = n_out + __popc(insm & lanemask_lt());
 #pragma unroll
-                        for (int w = 0; w < V; w++) outq[p * V + w] = key[u][w];
+                        for (int w = 0; w < V; w++) outq[p * V + w] = key[w];
                     }
                     n_out += __popc(insm);
                 }
@@ -419,49 +438,72 @@ static flat_kernel_t pick_flat(int v) {
 }
 
 // FINDORPUT + append of INSERTED keys (the receive side of the exchange)
+template <int V>
+__device__ __forceinline__ void append_keys(unsigned long long* ctr, uint32_t* out, uint64_t cap,
+                                            bool ins, const uint32_t* key) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t insm = __ballot_sync(FULLMASK, ins);
+    if (!insm) return;
+    unsigned long long pos0 = 0;
+    if (lane == 0) pos0 = atomicAdd(&ctr[0], (unsigned long long)__popc(insm));
+    pos0 = __shfl_sync(FULLMASK, pos0, 0);
+    if (ins) {
+        const unsigned long long p = pos0 + __popc(insm & lanemask_lt());
+        if (p < cap)
+            store_state<V>(out + p * V, key);
+        else
+            atomicExch(&ctr[2], 1ull);
+    }
+}
+
+// FINDORPUT + append of INSERTED keys (the receive side of the exchange)
 template <int BW, int V, int G, bool MARK>
 __global__ void __launch_bounds__(256) k_insert_append(TableDesc T, const uint32_t* __restrict__ keys,
                                                        uint64_t n, uint32_t* out, uint64_t cap,
                                                        unsigned long long* ctr) {
     // ctr: [0] appended, [1] table full, [2] overflow
     const int lane = threadIdx.x & 31;
-    constexpr int R = MARK ? 32 / G : 32;
-    const int grp = MARK ? lane / G : lane;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-    for (uint64_t base = warp * R; base < n; base += nwarps * R) {
-        const uint64_t e = base + grp;
-        const bool active = e < n;
-        uint32_t key[V];
+    bool any_full = false;
+    if constexpr (MARK) {
+        using S = ProbeShape<BW, G>;
+        const bool leader = (lane & (G - 1)) == 0;
+        for (uint64_t base = warp * S::KB; base < n; base += nwarps * S::KB) {
+            uint32_t own_key[S::M][V];
+            bool own_act[S::M];
 #pragma unroll
-        for (int w = 0; w < V; w++) key[w] = active ? keys[e * V + w] : 0u;
-        const uint64_t h = fold<V>(T.salt, key);
-        int64_t hd;
-        int code;
-        bool leader;
-        if constexpr (MARK) {
-            code = probe_mark<BW, V, G>(T, active, key, h, &hd);
-            leader = active && (lane & (G - 1)) == 0;
-        } else {
-            code = active ? probe_status(T, key, h, &hd) : FOUND;
-            leader = active;
-        }
-        const bool ins = leader && code == INSERTED;
-        if (__any_sync(FULLMASK, leader && code == TABLE_FULL) && lane == 0) atomicExch(&ctr[1], 1ull);
-        const uint32_t insm = __ballot_sync(FULLMASK, ins);
-        if (insm) {
-            unsigned long long pos0 = 0;
-            if (lane == 0) pos0 = atomicAdd(&ctr[0], (unsigned long long)__popc(insm));
-            pos0 = __shfl_sync(FULLMASK, pos0, 0);
-            if (ins) {
-                const unsigned long long p = pos0 + __popc(insm & lanemask_lt());
-                if (p < cap)
-                    store_state<V>(out + p * V, key);
-                else
-                    atomicExch(&ctr[2], 1ull);
+            for (int mm = 0; mm < S::M; mm++) {
+                const uint64_t e = base + lane + 32 * mm;
+                own_act[mm] = e < n;
+#pragma unroll
+                for (int w = 0; w < V; w++) own_key[mm][w] = own_act[mm] ? keys[e * V + w] : 0u;
+            }
+            uint32_t key[S::U][V];
+            bool act[S::U];
+            int code[S::U];
+            int64_t hd[S::U];
+            probe_batch<BW, V, G>(T, own_key, own_act, key, act, code, hd);
+#pragma unroll
+            for (int u = 0; u < S::U; u++) {
+                any_full |= leader && act[u] && code[u] == TABLE_FULL;
+                append_keys<V>(ctr, out, cap, leader && act[u] && code[u] == INSERTED, key[u]);
             }
         }
+    } else {
+        for (uint64_t base = warp * 32; base < n; base += nwarps * 32) {
+            const uint64_t e = base + lane;
+            const bool act = e < n;
+            uint32_t key[V];
+#pragma unroll
+            for (int w = 0; w < V; w++) key[w] = act ? keys[e * V + w] : 0u;
+            int64_t hd;
+            const int code = act ? probe_status(T, key, fold<V>(T.salt, key), &hd) : -1;
+            any_full |= act && code == TABLE_FULL;
+            append_keys<V>(ctr, out, cap, act && code == INSERTED, key);
+        }
     }
+    if (__any_sync(FULLMASK, any_full) && lane == 0) atomicExch(&ctr[1], 1ull);
 }
 
 typedef void (*append_kernel_t)(TableDesc, const uint32_t*, uint64_t, uint32_t*, uint64_t,
@@ -562,39 +604,45 @@ __device__ __forceinline__ void bench_key(const BenchArgs& B, uint64_t e, uint32
 template <int BW, int V, int G, bool MARK>
 __global__ void __launch_bounds__(256) k_bench(TableDesc T, BenchArgs B) {
     const int lane = threadIdx.x & 31;
-    constexpr int U = MARK ? Batch<(MARK ? BW : 32), G>::U : 1;
-    constexpr int R = MARK ? 32 / G : 32;
-    const int grp = MARK ? lane / G : lane;
-    const bool leader = MARK ? (lane & (G - 1)) == 0 : true;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
     unsigned long long ins = 0, full = 0;
-    for (uint64_t base = warp * R * U; base < B.total; base += nwarps * R * U) {
-        bool act[U];
-        uint32_t key[U][V];
-        uint64_t h[U];
-        int code[U];
-        int64_t hd[U];
+    if constexpr (MARK) {
+        using S = ProbeShape<BW, G>;
+        const bool leader = (lane & (G - 1)) == 0;
+        for (uint64_t base = warp * S::KB; base < B.total; base += nwarps * S::KB) {
+            uint32_t own_key[S::M][V];
+            bool own_act[S::M];
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-            const uint64_t e = base + u * R + grp;
-            act[u] = e < B.total;
-            if (act[u])
-                bench_key<V>(B, e, key[u]);
-            else
+            for (int mm = 0; mm < S::M; mm++) {
+                const uint64_t e = base + lane + 32 * mm;
+                own_act[mm] = e < B.total;
+                if (own_act[mm])
+                    bench_key<V>(B, e, own_key[mm]);
+                else
 #pragma unroll
-                for (int w = 0; w < V; w++) key[u][w] = 0;
-            h[u] = fold<V>(T.salt, key[u]);
+                    for (int w = 0; w < V; w++) own_key[mm][w] = 0;
+            }
+            uint32_t key[S::U][V];
+            bool act[S::U];
+            int code[S::U];
+            int64_t hd[S::U];
+            probe_batch<BW, V, G>(T, own_key, own_act, key, act, code, hd);
+#pragma unroll
+            for (int u = 0; u < S::U; u++) {
+                ins += leader && act[u] && code[u] == INSERTED;
+                full += leader && act[u] && code[u] == TABLE_FULL;
+            }
         }
-        if constexpr (MARK) {
-            probe_mark_multi<BW, V, G, U>(T, act, key, h, code, hd);
-        } else {
-            code[0] = act[0] ? probe_status(T, key[0], h[0], &hd[0]) : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            ins += leader && act[u] && code[u] == INSERTED;
-            full += leader && act[u] && code[u] == TABLE_FULL;
+    } else {
+        for (uint64_t e = warp * 32 + lane; e < B.total + 31; e += nwarps * 32) {
+            if (e >= B.total) break;
+            uint32_t key[V];
+            bench_key<V>(B, e, key);
+            int64_t hd;
+            const int code = probe_status(T, key, fold<V>(T.salt, key), &hd);
+            ins += code == INSERTED;
+            full += code == TABLE_FULL;
         }
     }
     ins = warp_sum(ins);

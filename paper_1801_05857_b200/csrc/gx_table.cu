@@ -79,27 +79,26 @@ __global__ void __launch_bounds__(256) k_fop_mark(TableDesc T, const uint32_t* _
             }
         }
     } else {
-        constexpr int U = Batch<BW, G>::U;
-        constexpr int R = 32 / G;
-        for (uint64_t base = warp * R * U; base < n; base += nwarps * R * U) {
-            bool act[U];
-            uint32_t key[U][V];
-            uint64_t h[U];
-            int code[U];
-            int64_t hd[U];
+        using S = ProbeShape<BW, G>;
+        for (uint64_t base = warp * S::KB; base < n; base += nwarps * S::KB) {
+            uint32_t own_key[S::M][V];
+            bool own_act[S::M];
 #pragma unroll
-            for (int u = 0; u < U; u++) {
-                const uint64_t e = base + u * R + grp;
-                act[u] = e < n;
+            for (int mm = 0; mm < S::M; mm++) {
+                const uint64_t e = base + lane + 32 * mm;
+                own_act[mm] = e < n;
 #pragma unroll
-                for (int w = 0; w < V; w++) key[u][w] = act[u] ? keys[e * V + w] : 0u;
-                h[u] = fold<V>(T.salt, key[u]);
+                for (int w = 0; w < V; w++) own_key[mm][w] = own_act[mm] ? keys[e * V + w] : 0u;
             }
-            probe_mark_multi<BW, V, G, U>(T, act, key, h, code, hd);
+            uint32_t key[S::U][V];
+            bool act[S::U];
+            int code[S::U];
+            int64_t hd[S::U];
+            probe_batch<BW, V, G>(T, own_key, own_act, key, act, code, hd);
 #pragma unroll
-            for (int u = 0; u < U; u++) {
+            for (int u = 0; u < S::U; u++) {
                 if (act[u] && leader) {
-                    const uint64_t e = base + u * R + grp;
+                    const uint64_t e = base + u * S::R + grp;
                     if (codes) codes[e] = (uint8_t)code[u];
                     if (handles) handles[e] = hd[u];
                     ins += code[u] == INSERTED;
@@ -167,8 +166,9 @@ static fop_kernel_t pick_v(int v, int g) {
     return nullptr;
 }
 
-// default probe group: one 16-byte chunk per lane (a bucket per G lanes)
-int default_group(int bw) { return bw / 4; }
+// default probe group (lanes per bucket), from the round-1 sweep on B200:
+// 32-word buckets: 2 lanes x 64 B; smaller buckets: one lane per bucket
+int default_group(int bw) { return bw >= 32 ? 2 : (bw >= 16 ? 2 : 1); }
 
 static fop_kernel_t pick_fop(int bw, int v, int g) {
     switch (bw) {

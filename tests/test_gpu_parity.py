@@ -194,7 +194,13 @@ def test_explore_matches_reference(name):
                 assert rep.outcome == "COMPLETE"
                 continue
             if want["outcome"] == "TABLE_FULL":
-                # schedule dependent in the reference too: check the invariants
+                # placement (hence the fill cliff) is schedule dependent: a
+                # run may complete, then it must be exact; else invariants
+                if rep.outcome == "COMPLETE":
+                    b = g["bfs"]
+                    assert (rep.states, rep.transitions, rep.deadlocks_total) == \
+                        (b["states"], b["transitions"], b["deadlocks_total"])
+                    continue
                 assert rep.outcome == "TABLE_FULL"
                 assert 0 < rep.states < g["bfs"]["states"]
                 lines = dump.splitlines()
