@@ -58,9 +58,12 @@ def parse():
     ap.add_argument("--hash-functions", type=int, default=8)
     ap.add_argument("--load", type=float, default=0.5, help="target table load factor")
     ap.add_argument("--probe-group", type=int, default=0)
+    ap.add_argument("--cache-slots", type=int, default=4096,
+                    help="per-block shared-memory dedup cache entries (< 32 = off)")
     ap.add_argument("--cpu-sample", default="ring12")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--hash-bench", action="store_true", help="add the bw x fill sweep")
+    ap.add_argument("--no-hash-bench", action="store_true",
+                    help="skip the isolated hash-table sweeps (configs[1])")
     ap.add_argument("--e2e-steps", type=int, default=2)
     return ap.parse_args()
 
@@ -198,13 +201,24 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
-def hash_sweep(torch, peaks):
-    """Isolated FINDORPUT throughput vs bucket size and fill (configs[1])."""
+def s_bw(bw: int) -> int:
+    """Bytes one bucket probe moves, rounded up to a 32-byte sector."""
+    return max(32, 4 * bw)
+
+
+def hash_sweep(ra: dict):
+    """Isolated FINDORPUT throughput vs bucket size and fill (configs[1]):
+    an 8 GiB table of 1-word vectors (>> L2) filled step by step with fresh
+    random keys; at each fill f the next 2% of inserts and a lookup pass
+    over the same keys are timed.  K = 8 (the reference default) and K = 32
+    (fill >= 0.6 needs it).  Algorithmic bytes per op:
+    4 (key) + S(bw) (bucket) + 32 if inserted; frac against R(S(bw))."""
     from paper_1801_05857_b200.bench import device_insert_bench
     from paper_1801_05857_b200.hashtable import StateTable, TableConfig
     out = []
-    words = 1 << 31  # 8 GiB of slots: >> L2
+    words = 1 << 31
     for bw in (4, 8, 16, 32):
+        r_g = ra.get(s_bw(bw), {}).get("gbs")
         for k in (8, 32):
             t = StateTable(TableConfig(bucket_words=bw, num_hash_functions=k, capacity_words=words),
                            1, mark=(0, 31))
@@ -213,8 +227,7 @@ def hash_sweep(torch, peaks):
             for fill in (0.5, 0.6, 0.7, 0.8, 0.9):
                 target = int(fill * slots)
                 batch = int(0.02 * slots)
-                # untimed fill to (fill - 2%), then time the next 2% of inserts
-                if target - batch > done:
+                if target - batch > done:  # untimed fill to (fill - 2%)
                     r = device_insert_bench(t, target - batch - done, 1, seed=7, row_base=done)
                     done += r["inserted"]
                     if r["full"]:
@@ -223,12 +236,53 @@ def hash_sweep(torch, peaks):
                 r = device_insert_bench(t, batch, 1, seed=7, row_base=done)
                 done += r["inserted"]
                 look = device_insert_bench(t, batch, 1, seed=7, row_base=done - batch)
-                cell = {"bw": bw, "k": k, "fill": fill, "insert_ops_per_sec": r["ops_per_sec"],
-                        "lookup_ops_per_sec": look["ops_per_sec"], "table_full": bool(r["full"])}
-                out.append(cell)
+                ins_gbs = r["ops_per_sec"] * (4 + s_bw(bw) + 32) / 1e9
+                look_gbs = look["ops_per_sec"] * (4 + s_bw(bw)) / 1e9
+                out.append({"bw": bw, "k": k, "fill": fill,
+                            "insert_ops_per_sec": r["ops_per_sec"],
+                            "lookup_ops_per_sec": look["ops_per_sec"],
+                            "insert_gbs_alg": ins_gbs, "lookup_gbs_alg": look_gbs,
+                            "lookup_frac_of_random_roofline": look_gbs / r_g if r_g else None,
+                            "table_full": bool(r["full"])})
                 if r["full"]:
                     break
             t.close()
+    return out
+
+
+def duplication_sweep(ra: dict):
+    """The paper's Fig. 4 protocol (bench.py:90-114,120-202): 2^28 FINDORPUT
+    ops over total/d unique random 1-word vectors, globally shuffled, table
+    sized for <= 50% load at d = 1; bucket 4 ("Gh-cbs") vs 32 ("Gh")."""
+    from paper_1801_05857_b200.bench import (DuplicationSpec, device_insert_bench,
+                                             insert_bench_table_config)
+    from paper_1801_05857_b200.hashtable import StateTable
+    total = 1 << 28
+    out = []
+    for bw in (4, 8, 16, 32):
+        for d in (1, 10, 50, 100):
+            spec = DuplicationSpec(total=total, duplication=d, vector_length=1)
+            t = StateTable(insert_bench_table_config(spec, bw), 1, mark=(0, 31))
+            try:
+                r = device_insert_bench(t, total, d, seed=11)
+            finally:
+                t.close()
+            u = total // d
+            alg = (total * (4 + s_bw(bw)) + u * 32) / (r["ms"] / 1e3) / 1e9
+            r_g = ra.get(s_bw(bw), {}).get("gbs")
+            out.append({"bw": bw, "d": d, "ops_per_sec": r["ops_per_sec"], "inserted": r["inserted"],
+                        "found": r["found"], "gbs_alg": alg,
+                        "frac_of_random_roofline": alg / r_g if r_g else None})
+    return out
+
+
+def random_access(granularities=(32, 64, 128)):
+    from paper_1801_05857_b200.bench import random_access_roofline
+    out = {}
+    for g in granularities:
+        r = random_access_roofline(g)
+        c = random_access_roofline(g, with_cas=True)
+        out[g] = {"gbs": r["gbs"], "gbs_with_cas": c["gbs"], "segments_per_sec": r["segments_per_sec"]}
     return out
 
 
@@ -272,7 +326,8 @@ def main():
     cap = table_capacity(states_est, vlen, args.bucket_words, args.load)
     tcfg = TableConfig(bucket_words=args.bucket_words, num_hash_functions=args.hash_functions,
                        capacity_words=cap)
-    cfg = ExploreConfig(table=tcfg, detect_deadlocks=True, probe_group=args.probe_group)
+    cfg = ExploreConfig(table=tcfg, detect_deadlocks=True, probe_group=args.probe_group,
+                        cache_slots=max(1, args.cache_slots))
     stream = torch.cuda.current_stream().cuda_stream
     ex = Explorer(net, cfg, stream=stream)
     table_bytes = ex.table.num_buckets * (4 * args.bucket_words + ((ex.table.slots_per_bucket + 7) & ~7))
@@ -299,8 +354,8 @@ def main():
     value = rep.states * args.steps / (ms / 1e3)
 
     # roofline of the dominant kernel (k_level), algorithmic bytes per step
-    s_bw = max(32, 4 * args.bucket_words)
-    alg_bytes = rep.transitions * s_bw + rep.states * 12 * vlen
+    sbw = s_bw(args.bucket_words)
+    alg_bytes = rep.transitions * sbw + rep.states * 12 * vlen
     level_ms = statistics.mean(r.level_ms for r in reps)
     achieved = alg_bytes / (level_ms / 1e3) / 1e9
     traffic = None
@@ -308,6 +363,9 @@ def main():
         tr = json.loads(TRAFFIC.read_text())
         traffic = tr.get(f"{args.workload}/bw{args.bucket_words}")
     ex.close()
+
+    # the random-access roofline R(g) on this GPU (32 GiB buffer >> L2)
+    ra = random_access()
 
     # e2e through the public API with host buffers
     torch.cuda.synchronize()
@@ -341,6 +399,7 @@ def main():
             "states": rep.states, "transitions": rep.transitions, "levels": rep.iterations - 1,
             "vector_words": vlen, "bucket_words": args.bucket_words,
             "hash_functions": args.hash_functions, "table_bytes": table_bytes,
+            "block_cache_slots": args.cache_slots,
             "load_factor": rep.states / ex.table.total_slots,
             "l2_policy": "table re-zeroed every step; table >> 126 MB L2",
             "parallelism": "single GPU",
@@ -349,7 +408,10 @@ def main():
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "kernel": "k_level", "algorithmic_bytes_per_step": alg_bytes,
                      "kernel_ms_per_step": level_ms,
-                     "bytes_model": "transitions*max(32,4*bw) + states*12*vlen"},
+                     "bytes_model": "transitions*max(32,4*bw) + states*12*vlen",
+                     "random_access_gbs": ra[sbw]["gbs"],
+                     "frac_of_random_access": achieved / ra[sbw]["gbs"],
+                     "random_access": ra},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": csr_bytes,
                 "d2h_bytes_per_step": 64 + 400 * vlen,
@@ -358,8 +420,8 @@ def main():
         "clocks": clocks.summary(),
         "probes_per_step": rep.probes,
     }
-    if args.hash_bench:
-        line["hash_bench"] = hash_sweep(torch, peaks)
+    if not args.no_hash_bench:
+        line["hash_bench"] = {"fill_sweep": hash_sweep(ra), "duplication_sweep": duplication_sweep(ra)}
     print(json.dumps(line), flush=True)
 
 

@@ -168,8 +168,13 @@ typedef struct gx_explore_cfg {
     int64_t max_iterations;     /* <= 0: none */
     uint64_t frontier_capacity; /* vectors; 0 = size from free device memory */
     int32_t probe_group;        /* 0 = auto; else lanes per bucket probe (1,2,4,8) */
-    int32_t reserved1;
+    int32_t cache_slots;        /* per-block shared-memory dedup cache entries (the
+                                   reference's LocalCache size, explore.py:91-144);
+                                   rounded down to a power of two, capped at
+                                   GX_CACHE_MAX_SLOTS; < 32 = off; vlen <= 2 only */
 } gx_explore_cfg;
+
+#define GX_CACHE_MAX_SLOTS 8192
 
 /* ExplorationReport (explore.py:65-88) */
 typedef struct gx_report {
@@ -230,6 +235,15 @@ int gx_bench_find_or_put(gx_table *t, uint64_t total, uint64_t duplication, uint
 int gx_bench_find_or_put_rows(gx_table *t, uint64_t total, uint64_t duplication, uint64_t row_base,
                               uint64_t seed, int32_t key_bits, int32_t probe_group, double *ms,
                               uint64_t *found, uint64_t *inserted, uint64_t *full);
+
+/* Random-access HBM roofline R(g) (SURVEY.md §8(d) denominator; no
+ * reference counterpart): `reads` aligned random reads of `granularity`
+ * bytes (16/32/64/128 = one bucket of bw 4/8/16/32) over a fresh device
+ * buffer of buffer_bytes (>> L2), best of `repeats` CUDA-event timed
+ * launches after one warm-up.  with_cas: also a 64-bit CAS on the first
+ * 8 bytes of every segment read as empty (the FINDORPUT insert path). */
+int gx_random_access_bench(uint64_t buffer_bytes, int32_t granularity, uint64_t reads,
+                           int32_t with_cas, int32_t repeats, double *ms_best, double *gbs_best);
 
 /* ----------------------------------------------------------------- misc */
 /* Insertion protocol chosen at create time: 0 = mark bit (single CAS),

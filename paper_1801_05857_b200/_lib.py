@@ -8,12 +8,15 @@ usable, every entry point raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 HERE = Path(__file__).resolve().parent
-LIB_PATH = HERE / "libgx.so"
+# GX_LIB (developer knob): load an alternative build of libgx.so, e.g. a
+# variant compiled with other tile constants for an A/B sweep
+LIB_PATH = Path(os.environ["GX_LIB"]) if os.environ.get("GX_LIB") else HERE / "libgx.so"
 
 GX_OK, GX_EINPUT, GX_ETABLE_FULL, GX_EINTERNAL = 0, 1, 2, 3
 
@@ -36,7 +39,7 @@ class NetworkCsr(C.Structure):
 class ExploreCfg(C.Structure):
     _fields_ = [("detect_deadlocks", C.c_int32), ("reserved0", C.c_int32),
                 ("max_iterations", C.c_int64), ("frontier_capacity", C.c_uint64),
-                ("probe_group", C.c_int32), ("reserved1", C.c_int32)]
+                ("probe_group", C.c_int32), ("cache_slots", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -86,6 +89,8 @@ SIGNATURES = {
     "gx_bench_find_or_put_rows": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                             C.c_int32, C.c_int32, _P(C.c_double), _u64p, _u64p,
                                             _u64p]),
+    "gx_random_access_bench": (C.c_int, [C.c_uint64, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
+                                         _P(C.c_double), _P(C.c_double)]),
     "gx_last_error": (C.c_char_p, []),
     "gx_kernel_launches": (C.c_uint64, []),
     "gx_device_info": (C.c_int, [_i32p, _u64p, _u64p]),

@@ -136,6 +136,17 @@ def device_insert_bench(table: StateTable, total: int, duplication: int = 1, see
             "ops_per_sec": total / (ms.value / 1e3) if ms.value > 0 else 0.0}
 
 
+def random_access_roofline(granularity: int, buffer_bytes: int = 32 << 30, reads: int = 1 << 28,
+                           with_cas: bool = False, repeats: int = 3) -> dict:
+    """R(g): aligned random g-byte reads over a buffer >> L2 (SURVEY.md
+    §8(d) denominator).  Returns {"g", "gbs", "ms", "segments_per_sec"}."""
+    ms, gbs = C.c_double(), C.c_double()
+    check(lib().gx_random_access_bench(buffer_bytes, granularity, reads, int(with_cas), repeats,
+                                       C.byref(ms), C.byref(gbs)))
+    return {"g": granularity, "gbs": gbs.value, "ms": ms.value, "with_cas": with_cas,
+            "segments_per_sec": reads / (ms.value / 1e3), "buffer_bytes": buffer_bytes}
+
+
 BENCH_CSV_COLUMNS = ("total", "duplication", "vector_length", "bucket_words", "threads", "seed",
                      "rep", "wall_ms", "inserts_per_sec", "found", "inserted")
 

@@ -11,7 +11,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 OUT = HERE / "libgx.so"
-SOURCES = ["gx_table.cu", "gx_explore.cu"]
+SOURCES = ["gx_table.cu", "gx_explore.cu", "gx_micro.cu"]
 NVCC_FLAGS = ["-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v", f"-I{HERE.parent / 'include'}"]
 
@@ -31,35 +31,40 @@ def stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: Path = OUT, defines=()) -> Path:
+    """Compile and link libgx.so (defines: extra -D flags for a variant build
+    written to `out`, used by the A/B sweep scripts)."""
+    if not force and out == OUT and not stale():
         return OUT
-    objdir = HERE / "build"
-    objdir.mkdir(exist_ok=True)
+    objdir = HERE / "build" / (out.stem if out != OUT else "")
+    objdir.mkdir(parents=True, exist_ok=True)
     procs = []
     for src in SOURCES:
         obj = objdir / (Path(src).stem + ".o")
         log = objdir / (Path(src).stem + ".ptxas.log")
-        cmd = [nvcc(), *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(CSRC / src), "-o", str(obj)]
         procs.append((cmd, obj, log, subprocess.Popen(cmd, stdout=subprocess.PIPE,
                                                       stderr=subprocess.STDOUT)))
     objs = []
     for cmd, obj, log, p in procs:
-        out, _ = p.communicate()
-        log.write_bytes(out)
+        txt, _ = p.communicate()
+        log.write_bytes(txt)
         if p.returncode != 0:
-            sys.stderr.write(out.decode(errors="replace")[-8000:])
+            sys.stderr.write(txt.decode(errors="replace")[-8000:])
             raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
         if verbose:
-            sys.stdout.write(out.decode(errors="replace"))
+            sys.stdout.write(txt.decode(errors="replace"))
         objs.append(str(obj))
-    tmp = OUT.with_suffix(".so.tmp")
+    tmp = out.with_suffix(".so.tmp")
     subprocess.run([nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs,
                     "-o", str(tmp)], check=True)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(OUT)
+    # python build.py [--force] [-v] [--out PATH -DNAME=VALUE ...]
+    argv = sys.argv[1:]
+    out = Path(argv[argv.index("--out") + 1]) if "--out" in argv else OUT
+    defs = [a[2:] for a in argv if a.startswith("-D")]
+    print(build(force="--force" in argv or out != OUT, verbose="-v" in argv, out=out, defines=defs))

@@ -334,12 +334,20 @@ __device__ __forceinline__ void probe_batch(const TableDesc& T,
             for (int j = 0; j < CPL; j++) ch[u][j] = ldcg4(base + 4 * (gl + j * G));
         }
     }
+    // masks of every key first, then the leaders' first-choice CASes issued
+    // back to back (independent atomics overlap instead of paying one L2
+    // round trip per key), then the verdicts; a lost first CAS re-judges
+    // the remaining EMPTY slots serially (rare).
+    constexpr int SPB = BW / V;
+    constexpr uint32_t ALL = SPB >= 32 ? 0xffffffffu : ((1u << SPB) - 1u);
+    uint32_t occ[U], match[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
         uint32_t km[V];
 #pragma unroll
         for (int w = 0; w < V; w++) km[w] = key[u][w] | (w == (int)T.mark_word ? T.mark : 0u);
-        uint32_t occ = 0, match = 0;
+        occ[u] = 0;
+        match[u] = 0;
         if (act[u]) {
 #pragma unroll
             for (int j = 0; j < CPL; j++) {
@@ -355,21 +363,67 @@ __device__ __forceinline__ void probe_batch(const TableDesc& T,
                         ob |= w4[t * V + w] & (w == (int)T.mark_word ? T.mark : 0u);
                         mm = mm && (w4[t * V + w] == km[w]);
                     }
-                    occ |= (ob != 0u ? 1u : 0u) << sl;
-                    match |= (mm ? 1u : 0u) << sl;
+                    occ[u] |= (ob != 0u ? 1u : 0u) << sl;
+                    match[u] |= (mm ? 1u : 0u) << sl;
                 }
             }
         }
 #pragma unroll
         for (int o = 1; o < G; o <<= 1) {
-            occ |= __shfl_xor_sync(FULLMASK, occ, o);
-            match |= __shfl_xor_sync(FULLMASK, match, o);
+            occ[u] |= __shfl_xor_sync(FULLMASK, occ[u], o);
+            match[u] |= __shfl_xor_sync(FULLMASK, match[u], o);
         }
-        int rc = -1;
+    }
+    int rc[U], slot[U];
+    uint32_t old[U][V];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        rc[u] = -1;
+        slot[u] = -1;
+        if (act[u] && gl == 0) {
+            if (match[u]) {
+                rc[u] = FOUND;
+                slot[u] = __ffs(match[u]) - 1;
+            } else {
+                const uint32_t empty = ~occ[u] & ALL;
+                if (empty) {
+                    uint32_t km[V];
+#pragma unroll
+                    for (int w = 0; w < V; w++) km[w] = key[u][w] | (w == (int)T.mark_word ? T.mark : 0u);
+                    slot[u] = __ffs(empty) - 1;
+                    SlotCas<V>::cas(T.data + bucket[u] * (uint64_t)BW + slot[u] * V, km, old[u]);
+                    rc[u] = -3;  // CAS in flight
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
         int64_t rh = -1;
-        if (act[u] && gl == 0) leader_resolve<BW, V>(T, bucket[u], occ, match, km, &rc, &rh);
-        if (G > 1) rc = __shfl_sync(FULLMASK, rc, leader);
-        code[u] = act[u] ? rc : -1;
+        if (rc[u] == -3) {
+            uint32_t km[V];
+            bool zero = true, eq = true;
+#pragma unroll
+            for (int w = 0; w < V; w++) {
+                km[w] = key[u][w] | (w == (int)T.mark_word ? T.mark : 0u);
+                zero = zero && old[u][w] == 0u;
+                eq = eq && old[u][w] == km[w];
+            }
+            if (zero) {
+                rc[u] = INSERTED;
+            } else if (eq) {
+                rc[u] = FOUND;
+            } else {
+                // lost the first EMPTY slot to another key: the rest in order
+                const uint32_t rest = ~occ[u] & ALL & ~((2u << slot[u]) - 1u);
+                leader_resolve<BW, V>(T, bucket[u], ~rest & ALL, 0u, km, &rc[u], &rh);
+                slot[u] = -1;
+            }
+        }
+        if (slot[u] >= 0) rh = (int64_t)(bucket[u] * (uint64_t)SPB + slot[u]);
+        int r = rc[u];
+        if (G > 1) r = __shfl_sync(FULLMASK, r, leader);
+        code[u] = act[u] ? r : -1;
         hd[u] = rh;
     }
 #pragma unroll

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "gx_expand.cuh"
+#include "gx_staged.cuh"
 #include "gx_internal.h"
 
 namespace gx {
@@ -26,6 +27,8 @@ struct LevelArgs {
     unsigned long long new_base, dl_base;
     uint32_t* dl;
     uint64_t dl_cap;
+    uint32_t cache_mask;  // block-local dedup cache slots - 1 (0 = no cache)
+    uint32_t pad;
 };
 
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
@@ -95,11 +98,60 @@ __device__ __forceinline__ void flush_out(const LevelArgs& A, const uint32_t* ou
     }
 }
 
+// Block-local dedup cache (GPUexplore's per-block cache; the
+// reference's LocalCache, explore.py:91-144): a direct-mapped table of
+// 64-bit packed keys (stored with the mark bit, so 0 = empty) in dynamic
+// shared memory.  atomicExch installs a key and returns the previous
+// occupant; only a key that was already there is dropped, because whoever
+// installed it has FINDORPUT it (or will) in this launch.  A forgotten key
+// just costs a global probe, so the cache never changes results.
+template <int V>
+__device__ __forceinline__ unsigned long long cache_word(const TableDesc& T, const uint32_t* key) {
+    unsigned long long kv = 0;
+#pragma unroll
+    for (int w = 0; w < V; w++)
+        kv |= (unsigned long long)(key[w] | (w == (int)T.mark_word ? T.mark : 0u)) << (32 * w);
+    return kv;
+}
+
+// Drop the successors in q[0, m) the block has already probed; survivors are
+// compacted to the front of q (stable).  Returns their number.
+template <int V>
+__device__ __forceinline__ uint32_t cache_filter(const TableDesc& T, unsigned long long* cache,
+                                                 uint32_t cmask, uint32_t* q, uint32_t m) {
+    const int lane = threadIdx.x & 31;
+    uint32_t kept = 0;
+    for (uint32_t r0 = 0; r0 < m; r0 += 32) {
+        const uint32_t e = r0 + lane;
+        const bool a = e < m;
+        uint32_t key[V];
+#pragma unroll
+        for (int w = 0; w < V; w++) key[w] = a ? q[e * V + w] : 0u;
+        bool keep = false;
+        if (a) {
+            const uint64_t h = fold<V>(T.salt, key);
+            const unsigned long long kv = cache_word<V>(T, key);
+            keep = atomicExch(&cache[(uint32_t)(h ^ (h >> 32)) & cmask], kv) != kv;
+        }
+        const uint32_t km = __ballot_sync(FULLMASK, keep);
+        __syncwarp();
+        if (keep) {
+            const uint32_t p = kept + __popc(km & lanemask_lt());
+#pragma unroll
+            for (int w = 0; w < V; w++) q[p * V + w] = key[w];
+        }
+        kept += __popc(km);
+        __syncwarp();
+    }
+    return kept;
+}
+
 // One BFS level.  Every warp takes 32 frontier states at a time:
 //   count pass   successors and transitions per state (expand_state),
 //                warp scan -> each lane's slice of the warp's successor list
 //   emit pass    successors into the warp's shared-memory queue, QWORDS/V
 //                at a time
+//   filter       (V <= 2) drop successors the block-local cache has seen
 //   probe        FINDORPUT of the queue: G lanes per key, U keys per lane
 //                group with all first-bucket loads issued up front
 //   stage        INSERTED keys go to a shared-memory out-queue, flushed to
@@ -113,8 +165,15 @@ __global__ void __launch_bounds__(256, GX_LEVEL_MINB) k_level(TableDesc T, NetDe
     constexpr int QCAP = QWORDS / V;
     __shared__ __align__(16) uint32_t qbuf[8][QWORDS];
     __shared__ __align__(16) uint32_t obuf[8][QWORDS];
+    extern __shared__ unsigned long long dcache[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
+    constexpr bool CACHE_OK = MARK && V <= 2;
+    const uint32_t cmask = CACHE_OK ? A.cache_mask : 0u;
+    if (cmask) {
+        for (uint32_t i = threadIdx.x; i <= cmask; i += blockDim.x) dcache[i] = 0ull;
+        __syncthreads();
+    }
     uint32_t* q = qbuf[wid];
     uint32_t* outq = obuf[wid];
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -154,7 +213,6 @@ __global__ void __launch_bounds__(256, GX_LEVEL_MINB) k_level(TableDesc T, NetDe
         }
         const uint32_t total = __shfl_sync(FULLMASK, incl, 31);
         const uint32_t excl = incl - n;
-        probes += lane == 0 ? total : 0;
         for (uint32_t c0 = 0; c0 < total; c0 += QCAP) {
             const uint32_t c1 = min(total, c0 + (uint32_t)QCAP);
             if (has && n && excl < c1 && excl + n > c0) {
@@ -164,7 +222,9 @@ __global__ void __launch_bounds__(256, GX_LEVEL_MINB) k_level(TableDesc T, NetDe
                 expand_state<V, true>(N, s, &dummy, lo, hi, q + (uint64_t)(excl + lo - c0) * V);
             }
             __syncwarp();
-            const uint32_t m = c1 - c0;
+            uint32_t m = c1 - c0;
+            if (CACHE_OK && cmask) m = cache_filter<V>(T, dcache, cmask, q, m);
+            probes += lane == 0 ? m : 0;
             uint32_t n_out = 0;
             bool any_full = false;
             if constexpr (MARK) {
@@ -231,6 +291,127 @@ __global__ void __launch_bounds__(256, GX_LEVEL_MINB) k_level(TableDesc T, NetDe
         if (expanded) atomicAdd(&A.ctr[LV_EXP], expanded);
         if (probes) atomicAdd(&A.ctr[LV_PROBES], probes);
     }
+}
+
+// The same level with the FINDORPUT of each successor chunk done by
+// probe_staged (gx_staged.cuh): bucket loads staged in shared memory with
+// cp.async, KB buckets in flight per warp.  All per-warp buffers live in
+// dynamic shared memory: [q 8*QWORDS u32][bucket idx 8*KB u64]
+// [stage 8*STAGE_BYTES][dedup cache].
+template <int BW, int V>
+struct StagedSmem {
+    using S = Staged<BW, V>;
+    static constexpr size_t Q = 8ull * QWORDS * 4;
+    static constexpr size_t B = 8ull * S::KB * 8;
+    static constexpr size_t ST = 8ull * S::STAGE_BYTES;
+    static constexpr size_t FIXED = Q + B + ST;
+};
+
+template <int BW, int V>
+__global__ void __launch_bounds__(256, 2) k_level_staged(TableDesc T, NetDesc N, LevelArgs A) {
+    using L = StagedSmem<BW, V>;
+    using S = Staged<BW, V>;
+    constexpr int QCAP = QWORDS / V;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * QWORDS;
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::KB;
+    uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
+    unsigned long long* dcache = reinterpret_cast<unsigned long long*>(smem + L::FIXED);
+    const uint32_t cmask = V <= 2 ? A.cache_mask : 0u;
+    if (cmask) {
+        for (uint32_t i = threadIdx.x; i <= cmask; i += blockDim.x) dcache[i] = 0ull;
+        __syncthreads();
+    }
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    unsigned long long trans = 0, expanded = 0, probes = 0;
+    for (uint64_t base = warp * 32; base < A.nfront; base += nwarps * 32) {
+        int stop = 0;
+        if (lane == 0)
+            stop = (*(volatile unsigned long long*)&A.ctr[LV_FULL] != 0ull) ||
+                   (*(volatile unsigned long long*)&A.ctr[LV_OVF] != 0ull);
+        if (__shfl_sync(FULLMASK, stop, 0)) break;
+        const uint64_t idx = base + lane;
+        const bool has = idx < A.nfront;
+        uint32_t s[V];
+        if (has)
+            load_state<V>(A.front + idx * V, s);
+        else
+#pragma unroll
+            for (int w = 0; w < V; w++) s[w] = 0;
+        uint64_t cnt = 0;
+        uint32_t n = 0;
+        if (has) {
+            n = expand_state<V, false>(N, s, &cnt, 0, 0, nullptr);
+            trans += cnt;
+            expanded += 1;
+            if (cnt == 0 && A.detect) {
+                unsigned long long p = atomicAdd(&A.ctr[LV_DL], 1ull) - A.dl_base;
+                if (p < A.dl_cap) store_state<V>(A.dl + p * V, s);
+            }
+        }
+        uint32_t incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(FULLMASK, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(FULLMASK, incl, 31);
+        const uint32_t excl = incl - n;
+        for (uint32_t c0 = 0; c0 < total; c0 += QCAP) {
+            const uint32_t c1 = min(total, c0 + (uint32_t)QCAP);
+            if (has && n && excl < c1 && excl + n > c0) {
+                const uint32_t lo = max(c0, excl) - excl;
+                const uint32_t hi = min(c1, excl + n) - excl;
+                uint64_t dummy;
+                expand_state<V, true>(N, s, &dummy, lo, hi, q + (uint64_t)(excl + lo - c0) * V);
+            }
+            __syncwarp();
+            uint32_t m = c1 - c0;
+            if (cmask) m = cache_filter<V>(T, dcache, cmask, q, m);
+            probes += lane == 0 ? m : 0;
+            bool full = false;
+            const uint32_t n_out = probe_staged<BW, V>(T, q, m, stage, sbkt, &full);
+            if (__any_sync(FULLMASK, full) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
+            if (n_out) flush_out<V>(A, q, n_out);
+            __syncwarp();
+        }
+    }
+    trans = warp_sum(trans);
+    expanded = warp_sum(expanded);
+    probes = warp_sum(probes);
+    if (lane == 0) {
+        if (trans) atomicAdd(&A.ctr[LV_TRANS], trans);
+        if (expanded) atomicAdd(&A.ctr[LV_EXP], expanded);
+        if (probes) atomicAdd(&A.ctr[LV_PROBES], probes);
+    }
+}
+
+struct LevelKernel {
+    void (*fn)(TableDesc, NetDesc, LevelArgs);
+    size_t fixed_smem;  // dynamic shared memory besides the dedup cache
+};
+
+template <int BW>
+static LevelKernel pick_staged_v(int v) {
+    switch (v) {
+        case 1: return {k_level_staged<BW, 1>, StagedSmem<BW, 1>::FIXED};
+        case 2: return {k_level_staged<BW, 2>, StagedSmem<BW, 2>::FIXED};
+        case 4: return {k_level_staged<BW, 4>, StagedSmem<BW, 4>::FIXED};
+    }
+    return {nullptr, 0};
+}
+
+static LevelKernel pick_staged(const TableDesc& T) {
+    switch (T.bw) {
+        case 4: return pick_staged_v<4>((int)T.vlen);
+        case 8: return pick_staged_v<8>((int)T.vlen);
+        case 16: return pick_staged_v<16>((int)T.vlen);
+        case 32: return pick_staged_v<32>((int)T.vlen);
+    }
+    return {nullptr, 0};
 }
 
 typedef void (*level_kernel_t)(TableDesc, NetDesc, LevelArgs);
@@ -861,11 +1042,32 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
     }
     cudaStream_t st = t->stream;
     const uint64_t launches0 = gx_kernel_launches();
-    level_kernel_t lk = pick_level(T, cfg->probe_group);
+    // probe_group 0 (auto) on in-band tables: the shared-memory staged
+    // level kernel; 1/2/4/8: the register-group kernel with that many lanes
+    // per bucket; status-byte tables: one lane per key
+    const bool staged = T.mode == MODE_MARK && cfg->probe_group == 0;
+    LevelKernel LK = staged ? pick_staged(T) : LevelKernel{pick_level(T, cfg->probe_group), 0};
+    level_kernel_t lk = LK.fn;
     if (!lk) {
         set_error("no level kernel for bw=%u vlen=%u group=%d", T.bw, v, cfg->probe_group);
         return GX_EINPUT;
     }
+    // block-local dedup cache: cache_slots rounded down to a power of two,
+    // at most GX_CACHE_MAX_SLOTS and what keeps two blocks per SM resident
+    // (only for in-band tables with vlen <= 2)
+    uint32_t cslots = 0;
+    if (cfg->cache_slots > 0 && T.mode == MODE_MARK && v <= 2) {
+        const size_t budget = 113 * 1024;  // dynamic smem per block at 2 blocks / SM
+        const size_t fixed = LK.fixed_smem + (staged ? 0 : 2 * 8 * QWORDS * 4);
+        cslots = 1;
+        while (cslots * 2 <= (uint32_t)cfg->cache_slots && cslots * 2 <= GX_CACHE_MAX_SLOTS &&
+               fixed + 8 * (size_t)cslots * 2 <= budget)
+            cslots *= 2;
+        if (cslots < 32) cslots = 0;
+    }
+    const size_t csmem = LK.fixed_smem + sizeof(unsigned long long) * cslots;
+    GX_CUDA(cudaFuncSetAttribute((const void*)lk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)csmem));
     int rc = gx_table_clear(t);
     if (rc) return rc;
     // frontier buffer: two-ended, capacity C vectors
@@ -937,10 +1139,12 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
                 A.dl_base = dl_base;
                 A.dl = (uint32_t*)n->dl.p;
                 A.dl_cap = dl_cap;
+                A.cache_mask = cslots ? cslots - 1 : 0;
+                A.pad = 0;
                 const uint64_t want = (nF + 31) / 32;  // warps
                 const int g = (int)std::min<uint64_t>((uint64_t)grid, (want + 7) / 8);
                 GX_CUDA(cudaEventRecord(la, st));
-                lk<<<g, 256, 0, st>>>(T, n->d, A);
+                lk<<<g, 256, csmem, st>>>(T, n->d, A);
                 GX_LAUNCHED();
                 GX_CUDA(cudaEventRecord(lb, st));
                 rep->levels_launched++;

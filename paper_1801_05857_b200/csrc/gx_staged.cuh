@@ -1,0 +1,240 @@
+// gx_staged.cuh -- FINDORPUT with the bucket loads staged in shared memory.
+//
+// The register-group probe (probe_batch, gx_device.cuh) holds every loaded
+// bucket in registers, so a warp can keep only ~32 buckets in flight and
+// the level kernel is latency bound (profiles/README.md, r1b: 19% of DRAM
+// peak, long-scoreboard stalls).  Here a warp stages a whole batch of KB
+// first buckets into its shared-memory slice with cp.async (LDGSTS,
+// L2-cached, no registers held while in flight), waits once, and then
+// every lane resolves its own keys from shared memory:
+//
+//   1. lane l owns keys l, l+32, ... of the batch: fold, first bucket
+//      (hashtable.py:205-217), bucket index -> per-warp smem array
+//   2. the warp copies the KB buckets (BW/4 16-byte chunks each, chunk j
+//      of key k at position j ^ (k mod CH): conflict-free LDS.128 later)
+//   3. each lane walks its buckets' slots in order: first slot equal to
+//      the key -> FOUND; first EMPTY slot -> CAS candidate (occupied slots
+//      are a bucket prefix, hashtable.py:229-231); none -> bucket full
+//   4. all candidates' CASes are issued back to back, then judged: lost to
+//      the same key -> FOUND, lost to another -> walk the rest of the
+//      bucket from global memory; full first bucket -> hash functions
+//      1..K-1 one lane per key (probe_lane; rare below the load cliff)
+//
+// Slot j of a bucket sits at word j*V for every layout the in-band mode
+// allows (vlen 1/2/4: the half layout's second half starts at bw/2, which
+// is exactly spb/2 slots in), so a bucket is scanned as a contiguous array.
+#pragma once
+#include "gx_device.cuh"
+
+#ifndef GX_STAGE_BYTES
+#define GX_STAGE_BYTES 8192  // shared-memory bucket staging per warp
+#endif
+#ifndef GX_STAGE_KB_MAX
+#define GX_STAGE_KB_MAX 128  // keys per staged batch at most
+#endif
+
+namespace gx {
+
+__device__ __forceinline__ uint32_t lanemask_lt_() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// A slot's words as one single-copy-atomic read (a torn read of a slot that
+// is being claimed could look like "another key" and let the key be
+// inserted twice further on).  V = 4 reads through a no-op CAS.
+template <int V>
+__device__ __forceinline__ void load_slot(uint32_t* p, uint32_t* out) {
+    if (V == 1) {
+        out[0] = __ldcg(p);
+    } else if (V == 2) {
+        const unsigned long long x = __ldcg(reinterpret_cast<const unsigned long long*>(p));
+        out[0] = (uint32_t)x;
+        out[1] = (uint32_t)(x >> 32);
+    } else {
+        const uint32_t zero[V] = {};
+        SlotCas<V>::cas(p, zero, out);
+    }
+}
+
+// One key, one lane: continue FINDORPUT in `bucket` from slot s0 on, reading
+// slots from global memory (after a lost CAS).  rc = -1 if the bucket fills.
+template <int BW, int V>
+__device__ __forceinline__ int resolve_lane_from(const TableDesc& T, uint64_t bucket, int s0,
+                                                 const uint32_t* km, int64_t* handle) {
+    constexpr int SPB = BW / V;
+    uint32_t* base = T.data + bucket * (uint64_t)BW;
+    for (int s = s0; s < SPB; s++) {
+        uint32_t cur[V];
+        load_slot<V>(base + s * V, cur);
+        bool zero = true;
+#pragma unroll
+        for (int w = 0; w < V; w++) zero = zero && cur[w] == 0u;
+        if (zero) {
+            if (SlotCas<V>::cas(base + s * V, km, cur)) {
+                *handle = (int64_t)(bucket * (uint64_t)SPB + s);
+                return INSERTED;
+            }
+        }
+        bool eq = true;
+#pragma unroll
+        for (int w = 0; w < V; w++) eq = eq && cur[w] == km[w];
+        if (eq) {
+            *handle = (int64_t)(bucket * (uint64_t)SPB + s);
+            return FOUND;
+        }
+    }
+    return -1;
+}
+
+// Hash functions i0..K-1 for one key, one lane (hashtable.py:237-280).
+template <int BW, int V>
+__device__ __forceinline__ int probe_lane(const TableDesc& T, const uint32_t* km, uint64_t h, int i0,
+                                          int64_t* handle) {
+    for (int i = i0; i < (int)T.k; i++) {
+        const int rc = resolve_lane_from<BW, V>(T, bucket_of(T, h, i), 0, km, handle);
+        if (rc >= 0) return rc;
+    }
+    *handle = -1;
+    return TABLE_FULL;
+}
+
+template <int BW, int V>
+struct Staged {
+    static constexpr int CH = BW / 4;                 // 16-byte chunks per bucket
+    static constexpr int SPB = BW / V;                // slots per bucket
+    static constexpr int SPC = 4 / V;                 // slots per chunk
+    static constexpr int STAGE_BYTES = GX_STAGE_BYTES;  // per warp
+    static constexpr int KB = STAGE_BYTES / (4 * BW) > GX_STAGE_KB_MAX ? GX_STAGE_KB_MAX
+                                                                       : STAGE_BYTES / (4 * BW);
+    static constexpr int KPL = KB / 32;               // keys per lane per batch
+};
+
+// FINDORPUT of keys q[0, m) (V words each, shared memory), KB at a time.
+// INSERTED keys are written back, compacted, to the front of q (a key is
+// only ever written at or below the position it was read from); returns
+// their number.  *full is set if any key hit TABLE_FULL.  stage: this
+// warp's STAGE_BYTES of shared memory; sbkt: its KB bucket indices.
+template <int BW, int V>
+__device__ __forceinline__ uint32_t probe_staged(const TableDesc& T, uint32_t* q, uint32_t m,
+                                                 uint4* stage, unsigned long long* sbkt,
+                                                 bool* full) {
+    using S = Staged<BW, V>;
+    constexpr int KB = S::KB, KPL = S::KPL, CH = S::CH, SPC = S::SPC;
+    const int lane = threadIdx.x & 31;
+    uint32_t n_ins = 0;
+    for (uint32_t r0 = 0; r0 < m; r0 += KB) {
+        const uint32_t nb = min((uint32_t)KB, m - r0);
+        uint32_t km[KPL][V];
+        uint64_t h[KPL], bkt[KPL];
+        bool act[KPL];
+#pragma unroll
+        for (int i = 0; i < KPL; i++) {
+            const uint32_t k = lane + 32 * i;
+            act[i] = k < nb;
+            uint32_t key[V];
+#pragma unroll
+            for (int w = 0; w < V; w++) key[w] = act[i] ? q[(r0 + k) * V + w] : 0u;
+            h[i] = fold<V>(T.salt, key);
+            bkt[i] = act[i] ? bucket_of(T, h[i], 0) : 0;
+#pragma unroll
+            for (int w = 0; w < V; w++) km[i][w] = key[w] | (w == (int)T.mark_word ? T.mark : 0u);
+            sbkt[k] = bkt[i];
+        }
+        __syncwarp();
+        // stage the first buckets: chunk c = key c / CH, part c % CH
+#pragma unroll
+        for (int it = 0; it < KPL * CH; it++) {
+            const uint32_t c = it * 32 + lane;
+            const uint32_t k = c / CH, j = c % CH;
+            if (k < nb)
+                cp_async16(stage + k * CH + (j ^ (k & (CH - 1))),
+                           T.data + sbkt[k] * (uint64_t)BW + 4 * j);
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        // walk each owned bucket from shared memory
+        int slot[KPL], rc[KPL];
+        uint32_t old[KPL][V];
+#pragma unroll
+        for (int i = 0; i < KPL; i++) {
+            const uint32_t k = lane + 32 * i;
+            slot[i] = -1;
+            rc[i] = -1;  // -1: bucket full, try the next hash function
+            if (!act[i]) continue;
+            for (int j = 0; j < CH && rc[i] == -1; j++) {
+                const uint4 c4 = stage[k * CH + (j ^ (k & (CH - 1)))];
+                const uint32_t w4[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+                for (int t = 0; t < SPC; t++) {
+                    if (rc[i] != -1) break;
+                    bool zero = true, eq = true;
+#pragma unroll
+                    for (int w = 0; w < V; w++) {
+                        zero = zero && w4[t * V + w] == 0u;
+                        eq = eq && w4[t * V + w] == km[i][w];
+                    }
+                    if (eq) {
+                        rc[i] = FOUND;
+                        slot[i] = j * SPC + t;
+                    } else if (zero) {
+                        rc[i] = -3;  // CAS candidate
+                        slot[i] = j * SPC + t;
+                    }
+                }
+            }
+        }
+        __syncwarp();  // stage and sbkt are free again
+        // the candidates' CASes back to back
+#pragma unroll
+        for (int i = 0; i < KPL; i++)
+            if (rc[i] == -3)
+                SlotCas<V>::cas(T.data + bkt[i] * (uint64_t)BW + slot[i] * V, km[i], old[i]);
+        bool ins[KPL];
+#pragma unroll
+        for (int i = 0; i < KPL; i++) {
+            int64_t hd;
+            if (rc[i] == -3) {
+                bool zero = true, eq = true;
+#pragma unroll
+                for (int w = 0; w < V; w++) {
+                    zero = zero && old[i][w] == 0u;
+                    eq = eq && old[i][w] == km[i][w];
+                }
+                if (zero)
+                    rc[i] = INSERTED;
+                else if (eq)
+                    rc[i] = FOUND;
+                else
+                    rc[i] = resolve_lane_from<BW, V>(T, bkt[i], slot[i] + 1, km[i], &hd);
+            }
+            if (act[i] && rc[i] == -1) rc[i] = probe_lane<BW, V>(T, km[i], h[i], 1, &hd);
+            ins[i] = act[i] && rc[i] == INSERTED;
+            *full |= act[i] && rc[i] == TABLE_FULL;
+        }
+        // INSERTED keys to the front of q, in key order
+#pragma unroll
+        for (int i = 0; i < KPL; i++) {
+            const uint32_t msk = __ballot_sync(FULLMASK, ins[i]);
+            if (ins[i]) {
+                const uint32_t p = n_ins + __popc(msk & lanemask_lt_());
+#pragma unroll
+                for (int w = 0; w < V; w++) q[p * V + w] = km[i][w] & ~(w == (int)T.mark_word ? T.mark : 0u);
+            }
+            n_ins += __popc(msk);
+        }
+        __syncwarp();
+    }
+    return n_ins;
+}
+
+}  // namespace gx

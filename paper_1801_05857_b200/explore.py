@@ -10,8 +10,12 @@ appends the inserted ones to the next frontier.  Rounds are exact BFS
 levels, so `iterations` = levels + 1 on a complete run, as in the
 reference (explore.py:234-240, 255-268).
 
-The CPU worker knobs (`workers`, `backend`, `cache_slots`) are accepted and
-validated for compatibility; they do not change device execution.
+`cache_slots` keeps its meaning as the size of the per-worker dedup cache
+(`LocalCache`, explore.py:91-144): on the device it sizes each thread
+block's shared-memory cache (rounded down to a power of two, at most
+8192; below 32 the cache is off).  The CPU worker knobs (`workers`,
+`backend`) are accepted and validated for compatibility; they do not change
+device execution.
 """
 
 from __future__ import annotations
@@ -164,7 +168,8 @@ class Explorer:
     def run(self) -> ExplorationReport:
         cfg = self.cfg
         ecfg = ExploreCfg(int(cfg.detect_deadlocks), 0, int(cfg.max_iterations or 0),
-                          int(cfg.frontier_capacity), int(cfg.probe_group), 0)
+                          int(cfg.frontier_capacity), int(cfg.probe_group),
+                          int(min(cfg.cache_slots, 1 << 30)))
         rep = Report()
         v = self.scheme.vector_length
         dl = np.zeros((DEADLOCK_KEEP, v), np.uint32)

@@ -274,6 +274,36 @@ def test_token_ring_closed_forms(n, tmp_path):
     assert rep.deadlocks_total == 0 and rep.outcome == "COMPLETE"
 
 
+@pytest.mark.parametrize("bw", [4, 8, 16, 32])
+@pytest.mark.parametrize("group,cache", [(0, 1), (0, 4096), (2, 4096)])
+def test_level_kernel_contention(bw, group, cache, tmp_path):
+    """Exact state count under heavy insert contention: token ring N=13
+    (4.78M states) in a table at load ~0.7 with K=32, so lost CASes, full
+    first buckets and the rehash path are all exercised, with and without
+    the block-local cache, staged (group 0) and register-group kernels."""
+    from paper_1801_05857_b200.bench import gen_token_ring
+    from paper_1801_05857_b200.hashtable import slots_per_bucket
+    n = 13
+    if group > 1 and bw < 8:
+        pytest.skip("group wider than the bucket")
+    _, p = gen_token_ring(n, tmp_path / "ring")
+    net = gx.load_network(p)
+    states = 2 * n * 3 ** (n - 1)
+    spb = slots_per_bucket(bw, 2, "half" if bw == 32 else "plain")
+    cap = (int(states / 0.7 / spb) + 64) * bw
+    cfg = ExploreConfig(table=TableConfig(bucket_words=bw, num_hash_functions=32, capacity_words=cap),
+                        detect_deadlocks=True, probe_group=group, cache_slots=cache)
+    ex = Explorer(net, cfg)
+    try:
+        for _ in range(2):
+            rep = ex.run()
+            assert (rep.states, rep.transitions, rep.outcome) == \
+                (states, 4 * n * n * 3 ** (n - 2), "COMPLETE")
+        assert ex.table.occupancy()[0] == states
+    finally:
+        ex.close()
+
+
 @pytest.mark.parametrize("kind,n", [("peterson", 3), ("peterson", 4), ("peterson", 5), ("gas", 9)])
 def test_generated_models_match_oracle(kind, n, tmp_path):
     from paper_1801_05857_b200.bench import gen_gas_station, gen_peterson
