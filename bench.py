@@ -301,7 +301,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_1801_05857_b200.distributed import bench_sharded
-        line = bench_sharded(args, torch, dist, model_path, closed_form, table_capacity)
+        line = bench_sharded(args, torch, dist, model_path, closed_form, table_capacity,
+                             ClockSampler(local))
         if rank == 0:
             print(json.dumps(line), flush=True)
         dist.destroy_process_group()

@@ -219,6 +219,46 @@ int gx_insert_append(gx_table *t, const uint32_t *d_keys, uint64_t n, uint32_t *
 int gx_owner_of(const gx_table *t, const uint32_t *keys, uint64_t n, int32_t ranks,
                 int32_t *owner);
 
+/* ------------------------------------------- fused sharded exploration */
+/* Hash-owner sharding across GPUs (the reference's
+ * nearest analogue is the bucket-range worker split, explore.py:284-286).
+ * One shard per GPU: shard `rank` owns the states with
+ * owner_of(fold) == rank and keeps them in table t.  Per BFS level the
+ * driver calls gx_shard_expand (expand the local frontier; successors owned
+ * by peers are stored straight into the peers' inboxes over NVLink,
+ * locally owned ones are FINDORPUT at once), then a barrier across ranks
+ * (e.g. an all_reduce), then gx_shard_absorb (FINDORPUT the inbox; stats
+ * of the level), then reduces the stats to decide termination exactly as
+ * explore.py:255-265 does.  Only in-band (mark bit) tables are supported. */
+typedef struct gx_shard gx_shard;
+#define GX_IPC_HANDLE_BYTES 64
+/* stats[] of gx_shard_absorb: per-level claims / new, then cumulative */
+#define GX_SH_CLAIMS 0
+#define GX_SH_NEW 1
+#define GX_SH_TRANSITIONS 2
+#define GX_SH_DEADLOCKS 3
+#define GX_SH_TABLE_FULL 4
+#define GX_SH_OVERFLOW 5
+#define GX_SH_ROUTED 6
+#define GX_SH_PROBES 7
+#define GX_SH_N 8
+int gx_shard_create(gx_net *n, gx_table *t, int32_t rank, int32_t world, uint64_t inbox_capacity,
+                    uint64_t frontier_capacity, int32_t cache_slots, gx_shard **out);
+int gx_shard_destroy(gx_shard *s);
+/* CUDA IPC handle of this shard's inbox (GX_IPC_HANDLE_BYTES bytes) */
+int gx_shard_ipc_handle(gx_shard *s, uint8_t *out);
+/* map every peer's inbox (world handles, rank order; own entry ignored) */
+int gx_shard_connect(gx_shard *s, const uint8_t *handles);
+/* all shards of one process (one GPU or several): connect them directly */
+int gx_shard_connect_local(gx_shard *const *shards, int32_t world);
+/* clear the shard's table; insert the initial state if this rank owns it */
+int gx_shard_begin(gx_shard *s, int32_t owns_initial, int32_t detect_deadlocks, int32_t *table_full);
+int gx_shard_expand(gx_shard *s);
+int gx_shard_absorb(gx_shard *s, uint64_t *stats);
+/* finalise statuses; local report (states, transitions, expanded,
+ * deadlocks of this shard; level_ms = its device time) */
+int gx_shard_finish(gx_shard *s, gx_report *report, uint32_t *deadlocks);
+
 /* ------------------------------------------------------------ benchmark */
 /* Isolated FINDORPUT benchmark (bench.py:120-202 protocol on device
  * generated keys): `total` operations, each unique vector repeated

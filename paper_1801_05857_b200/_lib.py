@@ -91,6 +91,16 @@ SIGNATURES = {
                                             _u64p]),
     "gx_random_access_bench": (C.c_int, [C.c_uint64, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
                                          _P(C.c_double), _P(C.c_double)]),
+    "gx_shard_create": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_uint64, C.c_uint64, C.c_int32,
+                                  _P(_vp)]),
+    "gx_shard_destroy": (C.c_int, [_vp]),
+    "gx_shard_ipc_handle": (C.c_int, [_vp, _u8p]),
+    "gx_shard_connect": (C.c_int, [_vp, _u8p]),
+    "gx_shard_connect_local": (C.c_int, [_P(_vp), C.c_int32]),
+    "gx_shard_begin": (C.c_int, [_vp, C.c_int32, C.c_int32, _i32p]),
+    "gx_shard_expand": (C.c_int, [_vp]),
+    "gx_shard_absorb": (C.c_int, [_vp, _u64p]),
+    "gx_shard_finish": (C.c_int, [_vp, _P(Report), _u32p]),
     "gx_last_error": (C.c_char_p, []),
     "gx_kernel_launches": (C.c_uint64, []),
     "gx_device_info": (C.c_int, [_i32p, _u64p, _u64p]),

@@ -11,7 +11,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 OUT = HERE / "libgx.so"
-SOURCES = ["gx_table.cu", "gx_explore.cu", "gx_micro.cu"]
+SOURCES = ["gx_table.cu", "gx_explore.cu", "gx_micro.cu", "gx_shard.cu"]
 NVCC_FLAGS = ["-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v", f"-I{HERE.parent / 'include'}"]
 

@@ -107,4 +107,6 @@ namespace gx {
 int table_find_or_put_dev(gx_table* t, const uint32_t* d_keys, uint64_t n, uint8_t* d_codes,
                           int64_t* d_handles, int serial, int group);
 int table_fixup_status(gx_table* t, const uint32_t* d_new_keys, uint64_t n_new);
+// keep the GX_DEADLOCK_KEEP smallest deadlock states (composite order)
+void keep_smallest(const gx_net* n, std::vector<uint32_t>& kept, const uint32_t* add, uint64_t cnt);
 }  // namespace gx

@@ -1,0 +1,347 @@
+// gx_level.cuh -- the pieces of one BFS level shared by the single-GPU
+// explorer (gx_explore.cu) and the hash-owner sharded one (gx_shard.cu):
+// level arguments and counters, frontier staging, the block-local dedup
+// cache, owner routing and the staged level body (expand -> cache ->
+// [route] -> FINDORPUT -> next frontier).  Reference: explore.py:147-281,
+// network.py:184-238, hashtable.py:224-280.
+#pragma once
+#include "gx_expand.cuh"
+#include "gx_staged.cuh"
+#include "gx_internal.h"
+
+namespace gx {
+
+// level counters live in the table's counter block
+enum { LV_NEW = 8, LV_TRANS = 9, LV_EXP = 10, LV_DL = 11, LV_FULL = 12, LV_OVF = 13, LV_PROBES = 14, LV_ROUTED = 15 };
+
+struct LevelArgs {
+    const uint32_t* front;
+    uint64_t nfront;
+    uint32_t* out;        // next frontier region base
+    uint64_t out_cap;     // vectors in the two-ended frontier buffer
+    uint64_t out_limit;   // max vectors F' may take (cap - |F|)
+    int32_t out_rev;      // F' position p lives at out[rev ? cap-1-p : p]
+    int32_t detect;
+    unsigned long long* ctr;
+    unsigned long long new_base, dl_base;
+    uint32_t* dl;
+    uint64_t dl_cap;
+    uint32_t cache_mask;  // block-local dedup cache slots - 1 (0 = no cache)
+    uint32_t pad;
+};
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+    return v;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <int V>
+__device__ __forceinline__ void load_state(const uint32_t* p, uint32_t* s) {
+    if (V == 1) {
+        s[0] = __ldcs(p);
+    } else if (V == 2) {
+        uint2 x = __ldcs(reinterpret_cast<const uint2*>(p));
+        s[0] = x.x;
+        s[1] = x.y;
+    } else if (V == 4) {
+        uint4 x = __ldcs(reinterpret_cast<const uint4*>(p));
+        s[0] = x.x;
+        s[1] = x.y;
+        s[2] = x.z;
+        s[3] = x.w;
+    } else {
+#pragma unroll
+        for (int w = 0; w < V; w++) s[w] = __ldcs(p + w);
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void store_state(uint32_t* p, const uint32_t* s) {
+    if (V == 2) {
+        *reinterpret_cast<uint2*>(p) = make_uint2(s[0], s[1]);
+    } else if (V == 4) {
+        *reinterpret_cast<uint4*>(p) = make_uint4(s[0], s[1], s[2], s[3]);
+    } else {
+#pragma unroll
+        for (int w = 0; w < V; w++) p[w] = s[w];
+    }
+}
+
+// words of shared memory per warp for the successor queue, and the same
+// again for the queue of freshly inserted keys (next-frontier staging)
+constexpr int QWORDS = 512;
+
+// Copy the warp's staged next-frontier keys to global memory with one
+// atomic per flush (the counter is shared by the whole grid).
+template <int V>
+__device__ __forceinline__ void flush_out(const LevelArgs& A, const uint32_t* outq, uint32_t n_out) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long pos0 = 0;
+    if (lane == 0) pos0 = atomicAdd(&A.ctr[LV_NEW], (unsigned long long)n_out) - A.new_base;
+    pos0 = __shfl_sync(FULLMASK, pos0, 0);
+    if (pos0 + n_out > A.out_limit) {
+        if (lane == 0) atomicExch(&A.ctr[LV_OVF], 1ull);
+        return;
+    }
+    for (uint32_t x = lane; x < n_out; x += 32) {
+        const unsigned long long p = pos0 + x;
+        const uint64_t slot = A.out_rev ? A.out_cap - 1 - p : p;
+        store_state<V>(A.out + slot * V, outq + (uint64_t)x * V);
+    }
+}
+
+// Block-local dedup cache (GPUexplore's per-block cache; the
+// reference's LocalCache, explore.py:91-144): a direct-mapped table of
+// 64-bit packed keys (stored with the mark bit, so 0 = empty) in dynamic
+// shared memory.  atomicExch installs a key and returns the previous
+// occupant; only a key that was already there is dropped, because whoever
+// installed it has FINDORPUT it (or will) in this launch.  A forgotten key
+// just costs a global probe, so the cache never changes results.
+template <int V>
+__device__ __forceinline__ unsigned long long cache_word(const TableDesc& T, const uint32_t* key) {
+    unsigned long long kv = 0;
+#pragma unroll
+    for (int w = 0; w < V; w++)
+        kv |= (unsigned long long)(key[w] | (w == (int)T.mark_word ? T.mark : 0u)) << (32 * w);
+    return kv;
+}
+
+// Drop the successors in q[0, m) the block has already probed; survivors are
+// compacted to the front of q (stable).  Returns their number.
+template <int V>
+__device__ __forceinline__ uint32_t cache_filter(const TableDesc& T, unsigned long long* cache,
+                                                 uint32_t cmask, uint32_t* q, uint32_t m) {
+    const int lane = threadIdx.x & 31;
+    uint32_t kept = 0;
+    for (uint32_t r0 = 0; r0 < m; r0 += 32) {
+        const uint32_t e = r0 + lane;
+        const bool a = e < m;
+        uint32_t key[V];
+#pragma unroll
+        for (int w = 0; w < V; w++) key[w] = a ? q[e * V + w] : 0u;
+        bool keep = false;
+        if (a) {
+            const uint64_t h = fold<V>(T.salt, key);
+            const unsigned long long kv = cache_word<V>(T, key);
+            keep = atomicExch(&cache[(uint32_t)(h ^ (h >> 32)) & cmask], kv) != kv;
+        }
+        const uint32_t km = __ballot_sync(FULLMASK, keep);
+        __syncwarp();
+        if (keep) {
+            const uint32_t p = kept + __popc(km & lanemask_lt());
+#pragma unroll
+            for (int w = 0; w < V; w++) q[p * V + w] = key[w];
+        }
+        kept += __popc(km);
+        __syncwarp();
+    }
+    return kept;
+}
+
+// ------------------------------------------------ hash-owner routing
+// Multi-GPU: rank `rank` of `world` owns the keys whose
+// owner_of(fold) is `rank`.  The level kernel routes every successor it
+// does not own straight into the owner's inbox over NVLink (peer pointers
+// from CUDA IPC; in one process, plain device pointers), reserving room
+// with one atomicAdd on the owner's inbox counter per (warp, owner,
+// chunk); successors it owns are probed locally right away.  The owners
+// FINDORPUT their inboxes after the level barrier (k_absorb, gx_shard.cu).
+#ifndef GX_MAX_SHARDS
+#define GX_MAX_SHARDS 16
+#endif
+
+struct RouteArgs {
+    uint32_t* inbox[GX_MAX_SHARDS];                 // peer r's inbox keys (V words each)
+    unsigned long long* inbox_ctr[GX_MAX_SHARDS];   // peer r's inbox fill counter
+    uint64_t inbox_cap;                             // keys per inbox
+    int32_t world, rank;
+};
+
+// Send the keys of q[0, m) owned by other ranks to their inboxes; the
+// locally owned ones are compacted (stably) to the front of q.  Returns
+// their number; *routed counts keys sent (lane 0).
+template <int V>
+__device__ __forceinline__ uint32_t route_remote(const TableDesc& T, const RouteArgs& R, uint32_t* q,
+                                                 uint32_t m, unsigned long long* ovf,
+                                                 unsigned long long* routed) {
+    const int lane = threadIdx.x & 31;
+    const int world = R.world;
+    // pass 1: lane r counts the chunk's keys owned by rank r
+    uint32_t cnt = 0;
+    for (uint32_t r0 = 0; r0 < m; r0 += 32) {
+        const uint32_t e = r0 + lane;
+        int o = -1;
+        if (e < m) {
+            uint32_t key[V];
+#pragma unroll
+            for (int w = 0; w < V; w++) key[w] = q[e * V + w];
+            o = owner_of(fold<V>(T.salt, key), world);
+        }
+        for (int r = 0; r < world; r++) {
+            const uint32_t b = __ballot_sync(FULLMASK, o == r);
+            if (lane == r) cnt += __popc(b);
+        }
+    }
+    // reserve room in every peer inbox at once (independent remote atomics)
+    unsigned long long base = 0;
+    bool ok = true;
+    if (lane < world && lane != R.rank && cnt) {
+        base = atomicAdd(R.inbox_ctr[lane], (unsigned long long)cnt);
+        if (base + cnt > R.inbox_cap) {
+            ok = false;
+            atomicExch(ovf, 1ull);
+        }
+    }
+    const uint32_t sent = __reduce_add_sync(FULLMASK, lane != R.rank && lane < world ? cnt : 0u);
+    if (lane == 0) *routed += sent;
+    // pass 2: scatter (peer stores, consecutive per owner) / compact local
+    uint32_t cur = 0, n_loc = 0;
+    for (uint32_t r0 = 0; r0 < m; r0 += 32) {
+        const uint32_t e = r0 + lane;
+        int o = -1;
+        uint32_t key[V];
+#pragma unroll
+        for (int w = 0; w < V; w++) key[w] = 0u;
+        if (e < m) {
+#pragma unroll
+            for (int w = 0; w < V; w++) key[w] = q[e * V + w];
+            o = owner_of(fold<V>(T.salt, key), world);
+        }
+        uint32_t pos = 0;
+        for (int r = 0; r < world; r++) {
+            const uint32_t b = __ballot_sync(FULLMASK, o == r);
+            const uint32_t at = __shfl_sync(FULLMASK, cur, r);
+            if (o == r) pos = at + __popc(b & lanemask_lt());
+            if (lane == r) cur += __popc(b);
+        }
+        const unsigned long long b_o = __shfl_sync(FULLMASK, base, o < 0 ? 0 : o);
+        const int ok_o = __shfl_sync(FULLMASK, ok ? 1 : 0, o < 0 ? 0 : o);
+        __syncwarp();
+        if (o >= 0 && o != R.rank) {
+            if (ok_o) {
+                uint32_t* dst = R.inbox[o] + (b_o + pos) * (uint64_t)V;
+#pragma unroll
+                for (int w = 0; w < V; w++) dst[w] = key[w];
+            }
+        } else if (o == R.rank) {
+            // pos counts this rank's keys so far: a stable in-place compaction
+#pragma unroll
+            for (int w = 0; w < V; w++) q[pos * V + w] = key[w];
+        }
+        __syncwarp();
+    }
+    n_loc = __shfl_sync(FULLMASK, cur, R.rank);
+    return n_loc;
+}
+
+// The same level with the FINDORPUT of each successor chunk done by
+// probe_staged (gx_staged.cuh): bucket loads staged in shared memory with
+// cp.async, KB buckets in flight per warp.  All per-warp buffers live in
+// dynamic shared memory: [q 8*QWORDS u32][bucket idx 8*KB u64]
+// [stage 8*STAGE_BYTES][dedup cache].
+template <int BW, int V>
+struct StagedSmem {
+    using S = Staged<BW, V>;
+    static constexpr size_t Q = 8ull * QWORDS * 4;
+    static constexpr size_t B = 8ull * S::KB * 8;
+    static constexpr size_t ST = 8ull * S::STAGE_BYTES;
+    static constexpr size_t FIXED = Q + B + ST;
+};
+
+template <int BW, int V, bool ROUTE>
+__device__ __forceinline__ void level_staged_body(const TableDesc& T, const NetDesc& N, const LevelArgs& A,
+                                                  const RouteArgs& R) {
+    using L = StagedSmem<BW, V>;
+    using S = Staged<BW, V>;
+    constexpr int QCAP = QWORDS / V;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * QWORDS;
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::KB;
+    uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
+    unsigned long long* dcache = reinterpret_cast<unsigned long long*>(smem + L::FIXED);
+    const uint32_t cmask = V <= 2 ? A.cache_mask : 0u;
+    if (cmask) {
+        for (uint32_t i = threadIdx.x; i <= cmask; i += blockDim.x) dcache[i] = 0ull;
+        __syncthreads();
+    }
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    unsigned long long trans = 0, expanded = 0, probes = 0, routed = 0;
+    for (uint64_t base = warp * 32; base < A.nfront; base += nwarps * 32) {
+        int stop = 0;
+        if (lane == 0)
+            stop = (*(volatile unsigned long long*)&A.ctr[LV_FULL] != 0ull) ||
+                   (*(volatile unsigned long long*)&A.ctr[LV_OVF] != 0ull);
+        if (__shfl_sync(FULLMASK, stop, 0)) break;
+        const uint64_t idx = base + lane;
+        const bool has = idx < A.nfront;
+        uint32_t s[V];
+        if (has)
+            load_state<V>(A.front + idx * V, s);
+        else
+#pragma unroll
+            for (int w = 0; w < V; w++) s[w] = 0;
+        uint64_t cnt = 0;
+        uint32_t n = 0;
+        if (has) {
+            n = expand_state<V, false>(N, s, &cnt, 0, 0, nullptr);
+            trans += cnt;
+            expanded += 1;
+            if (cnt == 0 && A.detect) {
+                unsigned long long p = atomicAdd(&A.ctr[LV_DL], 1ull) - A.dl_base;
+                if (p < A.dl_cap) store_state<V>(A.dl + p * V, s);
+            }
+        }
+        uint32_t incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(FULLMASK, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(FULLMASK, incl, 31);
+        const uint32_t excl = incl - n;
+        for (uint32_t c0 = 0; c0 < total; c0 += QCAP) {
+            const uint32_t c1 = min(total, c0 + (uint32_t)QCAP);
+            if (has && n && excl < c1 && excl + n > c0) {
+                const uint32_t lo = max(c0, excl) - excl;
+                const uint32_t hi = min(c1, excl + n) - excl;
+                uint64_t dummy;
+                expand_state<V, true>(N, s, &dummy, lo, hi, q + (uint64_t)(excl + lo - c0) * V);
+            }
+            __syncwarp();
+            uint32_t m = c1 - c0;
+            if (cmask) m = cache_filter<V>(T, dcache, cmask, q, m);
+            if (ROUTE) m = route_remote<V>(T, R, q, m, &A.ctr[LV_OVF], &routed);
+            probes += lane == 0 ? m : 0;
+            bool full = false;
+            const uint32_t n_out = probe_staged<BW, V>(T, q, m, stage, sbkt, &full);
+            if (__any_sync(FULLMASK, full) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
+            if (n_out) flush_out<V>(A, q, n_out);
+            __syncwarp();
+        }
+    }
+    trans = warp_sum(trans);
+    expanded = warp_sum(expanded);
+    probes = warp_sum(probes);
+    if (ROUTE) {
+        routed = warp_sum(routed);
+        __threadfence_system();  // peer inbox stores visible before the level barrier
+    }
+    if (lane == 0) {
+        if (ROUTE && routed) atomicAdd(&A.ctr[LV_ROUTED], routed);
+        if (trans) atomicAdd(&A.ctr[LV_TRANS], trans);
+        if (expanded) atomicAdd(&A.ctr[LV_EXP], expanded);
+        if (probes) atomicAdd(&A.ctr[LV_PROBES], probes);
+    }
+}
+
+}  // namespace gx

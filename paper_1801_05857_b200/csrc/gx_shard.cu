@@ -1,0 +1,422 @@
+// gx_shard.cu -- hash-owner sharded exploration.
+//
+// One gx_shard per GPU (or, for tests on one GPU, several per device in
+// one process).  Shard r owns the states with owner_of(fold) == r and
+// holds that part of the state table.  One BFS level is two kernels with a
+// cross-GPU barrier between them:
+//
+//   A  k_level_routed  expand the local frontier, drop block-cache hits,
+//                      store successors owned by peers straight into the
+//                      peers' inboxes (P2P stores over NVLink into
+//                      CUDA-IPC-mapped memory), FINDORPUT the locally
+//                      owned ones and append the inserted to the next
+//                      frontier -- the all-to-all is fused into the
+//                      expansion; no NCCL payload exchange, no staging
+//                      buffer
+//   -- barrier (the driver's all_reduce of the level counters) --
+//   B  k_absorb        FINDORPUT the keys peers sent, append the inserted
+//                      to the same next frontier
+//
+// Levels stay global BFS levels, so iterations / levels / transitions are
+// the single-GPU (and reference, explore.py:212-281) values.  The
+// reference's only parallelism is a bucket-range split of one shared
+// table between CPU workers (explore.py:284-286).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "gx_level.cuh"
+
+namespace gx {
+
+template <int BW, int V>
+__global__ void __launch_bounds__(256, 2) k_level_routed(TableDesc T, NetDesc N, LevelArgs A, RouteArgs R) {
+    level_staged_body<BW, V, true>(T, N, A, R);
+}
+
+// FINDORPUT the inbox (n = *count keys, clamped to cap); inserted keys go to
+// the next frontier through the level's LevelArgs.
+template <int BW, int V>
+__global__ void __launch_bounds__(256, 2) k_absorb(TableDesc T, LevelArgs A, const uint32_t* __restrict__ inbox,
+                                                  const unsigned long long* count, uint64_t cap) {
+    using L = StagedSmem<BW, V>;
+    using S = Staged<BW, V>;
+    constexpr int QCAP = QWORDS / V;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * QWORDS;
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::KB;
+    uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
+    unsigned long long* dcache = reinterpret_cast<unsigned long long*>(smem + L::FIXED);
+    const uint32_t cmask = V <= 2 ? A.cache_mask : 0u;
+    if (cmask) {
+        for (uint32_t i = threadIdx.x; i <= cmask; i += blockDim.x) dcache[i] = 0ull;
+        __syncthreads();
+    }
+    const uint64_t n = min((uint64_t)*count, cap);
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    unsigned long long probes = 0;
+    for (uint64_t base = warp * QCAP; base < n; base += nwarps * QCAP) {
+        const uint32_t m0 = (uint32_t)min((uint64_t)QCAP, n - base);
+        for (uint32_t x = lane; x < m0 * V; x += 32) q[x] = __ldcs(inbox + base * V + x);
+        __syncwarp();
+        uint32_t m = m0;
+        if (cmask) m = cache_filter<V>(T, dcache, cmask, q, m);
+        probes += lane == 0 ? m : 0;
+        bool full = false;
+        const uint32_t n_out = probe_staged<BW, V>(T, q, m, stage, sbkt, &full);
+        if (__any_sync(FULLMASK, full) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
+        if (n_out) flush_out<V>(A, q, n_out);
+        __syncwarp();
+    }
+    probes = warp_sum(probes);
+    if (lane == 0 && probes) atomicAdd(&A.ctr[LV_PROBES], probes);
+}
+
+typedef void (*routed_kernel_t)(TableDesc, NetDesc, LevelArgs, RouteArgs);
+typedef void (*absorb_kernel_t)(TableDesc, LevelArgs, const uint32_t*, const unsigned long long*, uint64_t);
+
+struct ShardKernels {
+    routed_kernel_t a;
+    absorb_kernel_t b;
+    size_t fixed_smem;
+};
+
+template <int BW>
+static ShardKernels pick_shard_v(int v) {
+    switch (v) {
+        case 1: return {k_level_routed<BW, 1>, k_absorb<BW, 1>, StagedSmem<BW, 1>::FIXED};
+        case 2: return {k_level_routed<BW, 2>, k_absorb<BW, 2>, StagedSmem<BW, 2>::FIXED};
+        case 4: return {k_level_routed<BW, 4>, k_absorb<BW, 4>, StagedSmem<BW, 4>::FIXED};
+    }
+    return {nullptr, nullptr, 0};
+}
+
+static ShardKernels pick_shard(const TableDesc& T) {
+    switch (T.bw) {
+        case 4: return pick_shard_v<4>((int)T.vlen);
+        case 8: return pick_shard_v<8>((int)T.vlen);
+        case 16: return pick_shard_v<16>((int)T.vlen);
+        case 32: return pick_shard_v<32>((int)T.vlen);
+    }
+    return {nullptr, nullptr, 0};
+}
+
+static constexpr size_t INBOX_HEAD = 256;  // counter cell, padded
+
+}  // namespace gx
+
+using namespace gx;
+
+struct gx_shard {
+    gx_net* n;
+    gx_table* t;
+    int32_t rank, world;
+    cudaStream_t stream;
+    ShardKernels K;
+    uint32_t cslots;
+    size_t smem;
+    // own inbox: [u64 counter | pad][keys]
+    void* inbox_block = nullptr;
+    uint64_t inbox_cap;
+    std::vector<void*> opened;  // peer blocks mapped through CUDA IPC
+    RouteArgs R;
+    bool connected = false;
+    // two-ended frontier buffer
+    DevBuf fb, dl;
+    uint64_t C;
+    const uint32_t* F = nullptr;
+    uint64_t nF = 0;
+    int rev = 1;
+    unsigned long long new_base = 0, dl_base = 0;
+    uint64_t dl_cap = 1 << 16;
+    uint64_t states = 0;
+    const uint32_t* pending = nullptr;
+    uint64_t n_pending = 0;
+    LevelArgs A;
+    std::vector<uint32_t> kept, dlhost;
+    cudaEvent_t e0, e1, e2;
+    double level_ms = 0;
+    int32_t detect = 0;
+};
+
+extern "C" {
+
+int gx_shard_create(gx_net* n, gx_table* t, int32_t rank, int32_t world, uint64_t inbox_capacity,
+                    uint64_t frontier_capacity, int32_t cache_slots, gx_shard** out) {
+    *out = nullptr;
+    const TableDesc& T = t->d;
+    if (world < 1 || world > GX_MAX_SHARDS || rank < 0 || rank >= world) {
+        set_error("shard rank %d / world %d outside 1..%d", rank, world, GX_MAX_SHARDS);
+        return GX_EINPUT;
+    }
+    if (T.vlen != n->vlen) {
+        set_error("table vector length %u != network vector length %u", T.vlen, n->vlen);
+        return GX_EINPUT;
+    }
+    if (T.mode != MODE_MARK) {
+        set_error("sharded exploration needs an in-band (mark bit) table; this packing has no spare bit");
+        return GX_EINPUT;
+    }
+    ShardKernels K = pick_shard(T);
+    if (!K.a) {
+        set_error("no sharded level kernel for bw=%u vlen=%u", T.bw, T.vlen);
+        return GX_EINPUT;
+    }
+    gx_shard* s = new gx_shard();
+    s->n = n;
+    s->t = t;
+    s->rank = rank;
+    s->world = world;
+    s->stream = t->stream;
+    s->K = K;
+    s->cslots = 0;
+    if (cache_slots > 0 && T.vlen <= 2) {
+        const size_t budget = 113 * 1024;
+        uint32_t c = 1;
+        while (c * 2 <= (uint32_t)cache_slots && c * 2 <= GX_CACHE_MAX_SLOTS && K.fixed_smem + 16 * (size_t)c <= budget)
+            c *= 2;
+        s->cslots = c >= 32 ? c : 0;
+    }
+    s->smem = K.fixed_smem + 8 * (size_t)s->cslots;
+    s->inbox_cap = std::max<uint64_t>(inbox_capacity, 1024);
+    s->C = std::max<uint64_t>(frontier_capacity, 1024);
+    memset(&s->R, 0, sizeof s->R);
+    s->R.world = world;
+    s->R.rank = rank;
+    s->R.inbox_cap = s->inbox_cap;
+    cudaError_t e = cudaMalloc(&s->inbox_block, INBOX_HEAD + sizeof(uint32_t) * s->inbox_cap * T.vlen);
+    if (e != cudaSuccess) {
+        set_error("inbox allocation (%llu keys) failed: %s", (unsigned long long)s->inbox_cap,
+                  cudaGetErrorString(e));
+        delete s;
+        return GX_EINTERNAL;
+    }
+    int rc = s->fb.ensure(sizeof(uint32_t) * s->C * T.vlen);
+    if (!rc) rc = s->dl.ensure(sizeof(uint32_t) * s->dl_cap * T.vlen);
+    if (rc) {
+        cudaFree(s->inbox_block);
+        delete s;
+        return rc;
+    }
+    GX_CUDA(cudaMemsetAsync(s->inbox_block, 0, INBOX_HEAD, s->stream));
+    GX_CUDA(cudaFuncSetAttribute((const void*)K.a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem));
+    GX_CUDA(cudaFuncSetAttribute((const void*)K.b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem));
+    GX_CUDA(cudaEventCreate(&s->e0));
+    GX_CUDA(cudaEventCreate(&s->e1));
+    GX_CUDA(cudaEventCreate(&s->e2));
+    *out = s;
+    return GX_OK;
+}
+
+int gx_shard_destroy(gx_shard* s) {
+    if (!s) return GX_OK;
+    cudaStreamSynchronize(s->stream);
+    for (void* p : s->opened) cudaIpcCloseMemHandle(p);
+    cudaFree(s->inbox_block);
+    s->fb.release();
+    s->dl.release();
+    cudaEventDestroy(s->e0);
+    cudaEventDestroy(s->e1);
+    cudaEventDestroy(s->e2);
+    delete s;
+    return GX_OK;
+}
+
+int gx_shard_ipc_handle(gx_shard* s, uint8_t* out) {
+    cudaIpcMemHandle_t h;
+    GX_CUDA(cudaIpcGetMemHandle(&h, s->inbox_block));
+    static_assert(sizeof(h) <= GX_IPC_HANDLE_BYTES, "IPC handle size");
+    memset(out, 0, GX_IPC_HANDLE_BYTES);
+    memcpy(out, &h, sizeof h);
+    return GX_OK;
+}
+
+static void set_peer(gx_shard* s, int r, void* block) {
+    s->R.inbox_ctr[r] = (unsigned long long*)block;
+    s->R.inbox[r] = (uint32_t*)((char*)block + INBOX_HEAD);
+}
+
+int gx_shard_connect(gx_shard* s, const uint8_t* handles) {
+    for (int r = 0; r < s->world; r++) {
+        if (r == s->rank) {
+            set_peer(s, r, s->inbox_block);
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, handles + (size_t)r * GX_IPC_HANDLE_BYTES, sizeof h);
+        void* p = nullptr;
+        GX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        s->opened.push_back(p);
+        set_peer(s, r, p);
+    }
+    s->connected = true;
+    return GX_OK;
+}
+
+int gx_shard_connect_local(gx_shard* const* shards, int32_t world) {
+    for (int i = 0; i < world; i++) {
+        gx_shard* s = shards[i];
+        if (s->world != world || s->rank != i) {
+            set_error("connect_local: shard %d has rank %d / world %d", i, s->rank, s->world);
+            return GX_EINPUT;
+        }
+        if (s->inbox_cap != shards[0]->inbox_cap) {
+            set_error("connect_local: inbox capacities differ");
+            return GX_EINPUT;
+        }
+        for (int r = 0; r < world; r++) set_peer(s, r, shards[r]->inbox_block);
+        s->connected = true;
+    }
+    return GX_OK;
+}
+
+int gx_shard_begin(gx_shard* s, int32_t owns_initial, int32_t detect_deadlocks, int32_t* table_full) {
+    if (!s->connected) {
+        set_error("shard not connected to its peers");
+        return GX_EINPUT;
+    }
+    gx_table* t = s->t;
+    int rc = gx_table_clear(t);
+    if (rc) return rc;
+    GX_CUDA(cudaMemsetAsync(s->inbox_block, 0, INBOX_HEAD, s->stream));
+    s->F = (const uint32_t*)s->fb.p;
+    s->nF = 0;
+    s->rev = 1;
+    s->new_base = s->dl_base = 0;
+    s->states = 0;
+    s->pending = nullptr;
+    s->n_pending = 0;
+    s->kept.clear();
+    s->level_ms = 0;
+    s->detect = detect_deadlocks;
+    *table_full = 0;
+    if (owns_initial) {
+        rc = t->codes.ensure(16);
+        if (rc) return rc;
+        rc = table_find_or_put_dev(t, s->n->d_initial, 1, (uint8_t*)t->codes.p, nullptr, 0, 0);
+        if (rc) return rc;
+        GX_CUDA(cudaMemcpyAsync(s->fb.p, s->n->d_initial, sizeof(uint32_t) * t->d.vlen,
+                                cudaMemcpyDeviceToDevice, s->stream));
+        uint8_t code0 = 0;
+        GX_CUDA(cudaMemcpyAsync(&code0, t->codes.p, 1, cudaMemcpyDeviceToHost, s->stream));
+        GX_CUDA(cudaStreamSynchronize(s->stream));
+        if (code0 == TABLE_FULL) {
+            *table_full = 1;
+        } else {
+            s->nF = 1;
+            s->states = 1;
+            s->pending = s->F;
+            s->n_pending = 1;
+        }
+    }
+    // the level counters restart from zero (the table clear zeroed them)
+    return GX_OK;
+}
+
+int gx_shard_expand(gx_shard* s) {
+    gx_table* t = s->t;
+    const uint32_t v = t->d.vlen;
+    LevelArgs& A = s->A;
+    A.front = s->F;
+    A.nfront = s->nF;
+    A.out = (uint32_t*)s->fb.p;
+    A.out_cap = s->C;
+    A.out_limit = s->C - s->nF;
+    A.out_rev = s->rev;
+    A.detect = s->detect;
+    A.ctr = (unsigned long long*)t->d_ctr;
+    A.new_base = s->new_base;
+    A.dl_base = s->dl_base;
+    A.dl = (uint32_t*)s->dl.p;
+    A.dl_cap = s->dl_cap;
+    A.cache_mask = s->cslots ? s->cslots - 1 : 0;
+    A.pad = 0;
+    (void)v;
+    GX_CUDA(cudaEventRecord(s->e0, s->stream));
+    if (s->nF) {
+        const uint64_t want = (s->nF + 31) / 32;
+        const int g = (int)std::min<uint64_t>((uint64_t)sm_count() * 2, (want + 7) / 8);
+        s->K.a<<<g, 256, s->smem, s->stream>>>(t->d, s->n->d, A, s->R);
+        GX_LAUNCHED();
+    }
+    GX_CUDA(cudaEventRecord(s->e1, s->stream));
+    return GX_OK;
+}
+
+int gx_shard_absorb(gx_shard* s, uint64_t* stats) {
+    gx_table* t = s->t;
+    const uint32_t v = t->d.vlen;
+    cudaStream_t st = s->stream;
+    // the inbox fill is only known on the device: a persistent grid that
+    // exits at once when nothing arrived
+    s->K.b<<<sm_count() * 2, 256, s->smem, st>>>(t->d, s->A, s->R.inbox[s->rank],
+                                                 s->R.inbox_ctr[s->rank], s->inbox_cap);
+    GX_LAUNCHED();
+    GX_CUDA(cudaEventRecord(s->e2, st));
+    unsigned long long* hc = (unsigned long long*)t->h_ctr;
+    unsigned long long inbox_n = 0;
+    GX_CUDA(cudaMemcpyAsync(hc, t->d_ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaMemcpyAsync(&inbox_n, s->R.inbox_ctr[s->rank], 8, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaMemsetAsync(s->R.inbox_ctr[s->rank], 0, 8, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    GX_CUDA(cudaEventElapsedTime(&ms, s->e0, s->e2));
+    s->level_ms += ms;
+    const uint64_t claims = s->nF;
+    const uint64_t nnew = hc[LV_NEW] - s->new_base;
+    s->new_base = hc[LV_NEW];
+    if (hc[LV_DL] > s->dl_base) {
+        const uint64_t d = std::min<uint64_t>(hc[LV_DL] - s->dl_base, s->dl_cap);
+        s->dlhost.resize(d * v);
+        GX_CUDA(cudaMemcpyAsync(s->dlhost.data(), s->dl.p, sizeof(uint32_t) * d * v, cudaMemcpyDeviceToHost, st));
+        GX_CUDA(cudaStreamSynchronize(st));
+        keep_smallest(s->n, s->kept, s->dlhost.data(), d);
+        s->dl_base = hc[LV_DL];
+    }
+    s->states += nnew;
+    const uint32_t* Fn = s->rev ? (const uint32_t*)s->fb.p + (s->C - nnew) * v : (const uint32_t*)s->fb.p;
+    s->pending = Fn;
+    s->n_pending = nnew;
+    s->F = Fn;
+    s->nF = nnew;
+    s->rev ^= 1;
+    // cumulative counters except claims / new (per level)
+    stats[GX_SH_CLAIMS] = claims;
+    stats[GX_SH_NEW] = nnew;
+    stats[GX_SH_TRANSITIONS] = hc[LV_TRANS];
+    stats[GX_SH_DEADLOCKS] = hc[LV_DL];
+    stats[GX_SH_TABLE_FULL] = hc[LV_FULL] ? 1 : 0;
+    stats[GX_SH_OVERFLOW] = (hc[LV_OVF] || inbox_n > s->inbox_cap) ? 1 : 0;
+    stats[GX_SH_ROUTED] = hc[LV_ROUTED];
+    stats[GX_SH_PROBES] = hc[LV_PROBES];
+    return GX_OK;
+}
+
+int gx_shard_finish(gx_shard* s, gx_report* rep, uint32_t* deadlocks) {
+    gx_table* t = s->t;
+    const uint32_t v = t->d.vlen;
+    int rc = table_fixup_status(t, s->pending, s->n_pending);
+    if (rc) return rc;
+    unsigned long long* hc = (unsigned long long*)t->h_ctr;
+    GX_CUDA(cudaMemcpyAsync(hc, t->d_ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost, s->stream));
+    GX_CUDA(cudaStreamSynchronize(s->stream));
+    memset(rep, 0, sizeof *rep);
+    rep->states = s->states;
+    rep->transitions = hc[LV_TRANS];
+    rep->expanded = hc[LV_EXP];
+    rep->deadlocks_total = hc[LV_DL];
+    rep->deadlocks_kept = (int32_t)(s->kept.size() / v);
+    rep->level_ms = s->level_ms;
+    rep->probes = hc[LV_PROBES];
+    if (deadlocks && !s->kept.empty()) memcpy(deadlocks, s->kept.data(), sizeof(uint32_t) * s->kept.size());
+    // occupancy counters of this shard's table after the run
+    unsigned long long cset[2] = {s->states, s->states - s->n_pending};
+    GX_CUDA(cudaMemcpyAsync(t->d_ctr, cset, sizeof cset, cudaMemcpyHostToDevice, s->stream));
+    GX_CUDA(cudaStreamSynchronize(s->stream));
+    return GX_OK;
+}
+
+}  // extern "C"

@@ -30,7 +30,7 @@
 #define GX_STAGE_BYTES 8192  // shared-memory bucket staging per warp
 #endif
 #ifndef GX_STAGE_KB_MAX
-#define GX_STAGE_KB_MAX 128  // keys per staged batch at most
+#define GX_STAGE_KB_MAX 64  // keys per staged batch at most (B200 sweep: 64 ~ 128 > 256)
 #endif
 
 namespace gx {
@@ -113,9 +113,9 @@ struct Staged {
     static constexpr int CH = BW / 4;                 // 16-byte chunks per bucket
     static constexpr int SPB = BW / V;                // slots per bucket
     static constexpr int SPC = 4 / V;                 // slots per chunk
-    static constexpr int STAGE_BYTES = GX_STAGE_BYTES;  // per warp
-    static constexpr int KB = STAGE_BYTES / (4 * BW) > GX_STAGE_KB_MAX ? GX_STAGE_KB_MAX
-                                                                       : STAGE_BYTES / (4 * BW);
+    static constexpr int KB = GX_STAGE_BYTES / (4 * BW) > GX_STAGE_KB_MAX ? GX_STAGE_KB_MAX
+                                                                          : GX_STAGE_BYTES / (4 * BW);
+    static constexpr int STAGE_BYTES = KB * 4 * BW;   // per warp
     static constexpr int KPL = KB / 32;               // keys per lane per batch
 };
 

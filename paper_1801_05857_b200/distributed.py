@@ -1,5 +1,15 @@
 """Hash-owner sharded exploration across GPUs (one process per GPU).
 
+Two drivers share the ownership rule and the level semantics:
+
+* the fused one (`FusedShard`, `explore_fused`, `explore_local_shards`;
+  gx_shard.cu): the level kernel routes successors owned by peers straight
+  into their inboxes over NVLink (CUDA IPC peer mappings) while it probes
+  its own, then every shard absorbs its inbox after a barrier -- the
+  all-to-all is fused into successor generation;
+* the collective one (`DeviceShard`, `explore_sharded`, below): expand,
+  bin by owner, NCCL all_to_all of counts and payload, insert.
+
 Every rank owns the states whose owner hash (a splitmix finaliser of the
 table's fold value, decorrelated from all bucket indices; gx_device.cuh
 `owner_of`) equals its rank, holds that shard of the state table, and
@@ -132,6 +142,216 @@ class DeviceShard:
         self.dnet.close()
 
 
+GX_SH = dict(claims=0, new=1, transitions=2, deadlocks=3, table_full=4, overflow=5, routed=6,
+             probes=7)
+IPC_HANDLE_BYTES = 64
+
+
+class FusedShard:
+    """One hash-owner shard on the fused level kernels (include/gx.h
+    gx_shard_*): the level kernel stores successors owned by peers straight
+    into their inboxes (P2P over NVLink, CUDA IPC mappings) and FINDORPUTs
+    its own; after the level barrier each shard absorbs its inbox."""
+
+    def __init__(self, net, cfg, rank: int, world: int, inbox_capacity: int = 0,
+                 frontier_capacity: int = 0, stream=None):
+        from . import statevec
+        from ._lib import check, lib
+        from .explore import DeviceNetwork
+        from .hashtable import StateTable
+
+        self.rank, self.world = rank, world
+        self.scheme = statevec.make_scheme(net)
+        self.vlen = self.scheme.vector_length
+        self.dnet = DeviceNetwork(net, self.scheme, stream)
+        self.table = StateTable(cfg.table, self.vlen, mark=statevec.mark_bit(self.scheme),
+                                stream=stream)
+        slots = self.table.total_slots
+        if not frontier_capacity:
+            sm, free, _tot = device_info()
+            frontier_capacity = max(1 << 16, min(slots + 2, int(free * 0.4) // (4 * self.vlen * world)))
+        if not inbox_capacity:
+            inbox_capacity = frontier_capacity
+        self.frontier_capacity, self.inbox_capacity = frontier_capacity, inbox_capacity
+        h = C.c_void_p()
+        check(lib().gx_shard_create(self.dnet.handle, self.table.handle, rank, world, inbox_capacity,
+                                    frontier_capacity, int(min(cfg.cache_slots, 1 << 30)),
+                                    C.byref(h)))
+        self._h = h
+        self.init = np.asarray(statevec.pack(self.scheme, net.initial), np.uint32)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def owner_of(self, packed: np.ndarray) -> int:
+        from ._lib import check, lib, ptr
+        arr = np.ascontiguousarray(packed, np.uint32).reshape(-1, self.vlen)
+        out = np.zeros(arr.shape[0], np.int32)
+        check(lib().gx_owner_of(self.table.handle, ptr(arr), arr.shape[0], self.world,
+                                ptr(out, C.c_int32)))
+        return int(out[0])
+
+    def ipc_handle(self) -> bytes:
+        from ._lib import check, lib, ptr
+        buf = np.zeros(IPC_HANDLE_BYTES, np.uint8)
+        check(lib().gx_shard_ipc_handle(self._h, ptr(buf, C.c_uint8)))
+        return buf.tobytes()
+
+    def connect(self, handles):
+        from ._lib import check, lib, ptr
+        buf = np.frombuffer(b"".join(handles), np.uint8).copy()
+        check(lib().gx_shard_connect(self._h, ptr(buf, C.c_uint8)))
+
+    def begin(self, detect: bool) -> bool:
+        """Clear; insert the initial state if owned.  True if TABLE_FULL."""
+        from ._lib import check, lib
+        full = C.c_int32()
+        owns = self.owner_of(self.init) == self.rank
+        check(lib().gx_shard_begin(self._h, int(owns), int(detect), C.byref(full)))
+        return bool(full.value)
+
+    def expand(self):
+        from ._lib import check, lib
+        check(lib().gx_shard_expand(self._h))
+
+    def absorb(self) -> np.ndarray:
+        from ._lib import check, lib, ptr
+        st = np.zeros(8, np.uint64)
+        check(lib().gx_shard_absorb(self._h, ptr(st, C.c_uint64)))
+        return st
+
+    def finish(self):
+        from . import statevec
+        from ._lib import Report, check, lib, ptr
+        rep = Report()
+        dl = np.zeros((100, self.vlen), np.uint32)
+        check(lib().gx_shard_finish(self._h, C.byref(rep), ptr(dl)))
+        kept = [statevec.unpack(self.scheme, tuple(int(x) for x in dl[i]))
+                for i in range(rep.deadlocks_kept)]
+        return rep, kept
+
+    def close(self):
+        from ._lib import lib
+        if getattr(self, "_h", None):
+            lib().gx_shard_destroy(self._h)
+            self._h = None
+        self.table.close()
+        self.dnet.close()
+
+
+def device_info():
+    from ._lib import lib
+    sm, free, tot = C.c_int32(), C.c_uint64(), C.c_uint64()
+    lib().gx_device_info(C.byref(sm), C.byref(free), C.byref(tot))
+    return sm.value, free.value, tot.value
+
+
+def connect_local(shards):
+    from ._lib import check, lib
+    arr = (C.c_void_p * len(shards))(*[s.handle.value for s in shards])
+    check(lib().gx_shard_connect_local(arr, len(shards)))
+
+
+def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None) -> ShardResult:
+    """The level protocol shared by the in-process and multi-process
+    drivers: every shard expands, a barrier, every shard absorbs, the
+    level's stats are reduced over all ranks (explore.py:251-265)."""
+    full = reduce(np.array([sum(int(s.begin(detect)) for s in shards)], np.uint64))[0]
+    rounds = 0
+    outcome = "COMPLETE"
+    if full:
+        outcome = "TABLE_FULL"
+    else:
+        while True:
+            for s in shards:
+                s.expand()
+            barrier()
+            st = np.zeros(8, np.uint64)
+            for s in shards:
+                st += s.absorb()
+            st = reduce(st)
+            rounds += 1
+            if st[GX_SH["overflow"]]:
+                raise RuntimeError("frontier or inbox capacity exceeded in sharded exploration; "
+                                   "raise frontier_capacity / inbox_capacity")
+            if st[GX_SH["table_full"]]:
+                outcome = "TABLE_FULL"
+                break
+            if st[GX_SH["claims"]] == 0:
+                break
+            if max_iterations and rounds >= max_iterations:
+                outcome = "ITERATION_CAP"
+                break
+    tot = np.zeros(5, np.uint64)
+    kept = []
+    for s in shards:
+        rep, k = s.finish()
+        tot += np.array([rep.states, rep.transitions, rep.expanded, rep.deadlocks_total, rep.probes],
+                        np.uint64)
+        kept.extend(k)
+    return tot, sorted(kept)[:100], rounds, outcome
+
+
+def explore_local_shards(net, cfg, world: int, inbox_capacity: int = 0, frontier_capacity: int = 0):
+    """Hash-owner sharded exploration with all `world` shards in this
+    process (one GPU): the multi-GPU protocol and kernels, with peer
+    inboxes as local device memory.  Returns an ExplorationReport; its
+    results equal explore(net, cfg)'s."""
+    import time
+
+    from .explore import ExplorationReport
+
+    shards = [FusedShard(net, cfg, r, world, inbox_capacity, frontier_capacity) for r in range(world)]
+    try:
+        connect_local(shards)
+        t0 = time.perf_counter()
+        tot, kept, rounds, outcome = _run_levels(shards, lambda: None, lambda a: a,
+                                                 cfg.detect_deadlocks, cfg.max_iterations)
+        wall = time.perf_counter() - t0
+        states = int(tot[0])
+        return ExplorationReport(
+            states=states, transitions=int(tot[1]), deadlocks=tuple(kept),
+            deadlocks_total=int(tot[3]), expanded=int(tot[2]), iterations=rounds, wall_time=wall,
+            throughput=states / wall if wall > 0 else 0.0, outcome=outcome, probes=int(tot[4]))
+    finally:
+        for s in shards:
+            s.close()
+
+
+def explore_fused(shard: FusedShard, dist, torch, detect: bool, max_iterations=None,
+                  device=None) -> ShardResult:
+    """Multi-process driver (one process per GPU): shards were connected
+    with their peers' IPC handles; the barrier and the stats reduction are
+    NCCL all_reduces on the shards' stream."""
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    flag = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def barrier():
+        dist.all_reduce(flag)
+
+    def reduce(a):
+        t = torch.from_numpy(a.astype(np.int64)).to(dev)
+        dist.all_reduce(t)
+        return t.cpu().numpy().astype(np.uint64)
+
+    tot, kept, rounds, outcome = _run_levels([shard], barrier, reduce, detect, max_iterations)
+    tot = reduce(tot)
+    gathered = [None] * dist.get_world_size()
+    dist.all_gather_object(gathered, kept)
+    dls = tuple(sorted(s for part in gathered for s in part)[:100])
+    return ShardResult(states=int(tot[0]), transitions=int(tot[1]), deadlocks=dls,
+                       deadlocks_total=int(tot[3]), expanded=int(tot[2]), iterations=rounds,
+                       outcome=outcome, levels=rounds - 1)
+
+
+def connect_fused(shard: FusedShard, dist):
+    """Exchange the shards' inbox IPC handles and map the peers'."""
+    handles = [None] * dist.get_world_size()
+    dist.all_gather_object(handles, shard.ipc_handle())
+    shard.connect(handles)
+
+
 def explore_sharded(backend, dist, torch, scheme, initial_packed: np.ndarray, detect: bool,
                     max_iterations=None, device=None) -> ShardResult:
     """Run the level loop of the module docstring on every rank."""
@@ -198,9 +418,13 @@ def explore_sharded(backend, dist, torch, scheme, initial_packed: np.ndarray, de
                        outcome=outcome, levels=rounds - 1)
 
 
-def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity):
-    """bench.py's N > 1 leg: strong scaling of one model over N GPUs."""
-    import statistics
+def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, clock_sampler=None):
+    """bench.py's N > 1 leg: one model hash-partitioned over N GPUs (strong
+    scaling), fused peer-routed levels.  Device time = CUDA events around
+    the K timed explorations, max over ranks; e2e = the same through
+    shard construction (CSR upload, table + inbox allocation, IPC mapping)
+    per step."""
+    import json as _json
     import tempfile
     import time
     from pathlib import Path
@@ -214,40 +438,87 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity):
     tmp = Path(tempfile.mkdtemp())
     net = load_network(model_path(args.workload, tmp))
     scheme = statevec.make_scheme(net)
+    vlen = scheme.vector_length
     cf = closed_form(args.workload)
-    per_rank = cf[0] // world + (cf[0] >> 6) + 1024
-    cap_words = table_capacity(per_rank, scheme.vector_length, args.bucket_words, args.load)
+    per_rank = cf[0] // world + (cf[0] >> 8) + 4096
+    cap_words = table_capacity(per_rank, vlen, args.bucket_words, args.load)
     cfg = ExploreConfig(table=TableConfig(bucket_words=args.bucket_words,
                                           num_hash_functions=args.hash_functions,
-                                          capacity_words=cap_words), detect_deadlocks=True)
+                                          capacity_words=cap_words), detect_deadlocks=True,
+                        cache_slots=max(1, args.cache_slots))
     dev = torch.device("cuda", torch.cuda.current_device())
-    backend = DeviceShard(net, cfg, world, torch, capacity=max(1 << 20, per_rank // 4),
-                          stream=torch.cuda.current_stream().cuda_stream)
-    init = np.asarray(statevec.pack(scheme, net.initial), np.uint32)
+    stream = torch.cuda.current_stream().cuda_stream
+    frontier = max(1 << 20, per_rank // 6)
+
+    def make():
+        sh = FusedShard(net, cfg, rank, world, inbox_capacity=frontier, frontier_capacity=frontier,
+                        stream=stream)
+        connect_fused(sh, dist)
+        return sh
+
+    shard = make()
     res = None
     for _ in range(args.warmup):
-        res = explore_sharded(backend, dist, torch, scheme, init, True, device=dev)
+        res = explore_fused(shard, dist, torch, True, device=dev)
     torch.cuda.synchronize()
     dist.barrier()
     l0 = _lib.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        res = explore_sharded(backend, dist, torch, scheme, init, True, device=dev)
-    e1.record()
-    torch.cuda.synchronize()
+    ctx = clock_sampler if clock_sampler is not None else _Null()
+    with ctx:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            res = explore_fused(shard, dist, torch, True, device=dev)
+        e1.record()
+        torch.cuda.synchronize()
     dist.barrier()
+    launches = _lib.kernel_launches() - l0
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
-    backend.close()
+    shard.close()
+    assert (res.states, res.transitions) == cf, (res.states, res.transitions, cf)
+    # e2e: shards built (CSR from host memory, tables, inboxes, IPC) every step
+    e2e = []
+    for i in range(args.e2e_steps + 1):
+        dist.barrier()
+        t0 = time.perf_counter()
+        sh = make()
+        r = explore_fused(sh, dist, torch, True, device=dev)
+        sh.close()
+        torch.cuda.synchronize()
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if i:
+            e2e.append(float(t.item()))
+    e2e_value = r.states * len(e2e) / sum(e2e) if e2e else None
     return {
         "metric": "states explored/sec", "value": res.states * args.steps / (ms / 1e3),
         "unit": "states/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (generated model, exact state space)",
-        "config": {"workload": args.workload, "states": res.states, "transitions": res.transitions,
-                   "levels": res.levels, "parallelism": f"hash-owner sharding x{world}, "
-                   "per-level NCCL all_to_all + all_reduce"},
-        "gpu_launches": _lib.kernel_launches() - l0,
+        "config": {"workload": f"configs[4] token ring N={args.workload[4:]} hash-partitioned",
+                   "states": res.states, "transitions": res.transitions, "levels": res.levels,
+                   "vector_words": vlen, "bucket_words": args.bucket_words,
+                   "hash_functions": args.hash_functions, "table_words_per_rank": cap_words,
+                   "block_cache_slots": args.cache_slots,
+                   "l2_policy": "tables re-zeroed every step; tables >> 126 MB L2",
+                   "parallelism": f"hash-owner sharding x{world}: successors routed to the owner's "
+                                  "inbox by P2P stores inside the level kernel (CUDA IPC over "
+                                  "NVLink), NCCL all_reduce of level counters"},
+        "roofline": None, "cpu_baseline": None,
+        "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": None,
+                "d2h_bytes_per_step": None,
+                "api": "FusedShard + connect_fused + explore_fused per step"},
+        "gpu_launches": launches,
+        "clocks": clock_sampler.summary() if clock_sampler is not None else None,
     }
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False

@@ -156,3 +156,133 @@ def test_sharded_iteration_cap_and_table_full():
     assert (states, trans, iters, outcome) == (cap.states, cap.transitions, 3, "ITERATION_CAP")
     name, states, _, _, _, _, outcome, _ = res[1]
     assert outcome == "TABLE_FULL" and 0 < states < 2916
+
+
+# ------------------------------------------------ fused (peer-routed) driver
+
+class OracleFusedShard:
+    """CPU stand-in for FusedShard (tests only).  expand() probes the
+    locally owned successors at once and stages the others per owner, as
+    k_level_routed does; the P2P inbox stores are emulated by a gloo
+    all_to_all inside absorb() (the device writes them during expand)."""
+
+    def __init__(self, path, table_kw, world, rank):
+        self.base = OracleShard(path, table_kw, world)
+        self.rank, self.world = rank, world
+        self.vlen = self.base.vlen
+        self.init = None
+
+    def begin(self, detect):
+        from paper_1801_05857_b200 import statevec
+        b = self.base
+        b.reset()
+        self.detect = detect
+        self.trans = self.dl_total = self.expanded = 0
+        self.kept = []
+        self.states = 0
+        self.front = np.zeros((0, self.vlen), np.uint32)
+        init = np.asarray(statevec.pack(b.scheme, b.net.initial), np.uint32)
+        if int(b.owner(init)[0]) == self.rank:
+            code, _ = b.table.find_or_insert(init)
+            if code == 2:
+                return True
+            self.front = init.reshape(1, -1)
+            self.states = 1
+        return False
+
+    def expand(self):
+        b = self.base
+        self.claims = len(self.front)
+        self.expanded += self.claims
+        succ = []
+        for row in self.front:
+            out, c = b.net.expand(b.net.unpack(row))
+            self.trans += c
+            if not out and self.detect:
+                self.dl_total += 1
+                self.kept.append(b.net.unpack(row))
+            succ += [b.net.pack(t) for _, t in out]
+        arr = np.array(succ, np.uint32).reshape(-1, self.vlen)
+        own = b.owner(arr) if len(arr) else np.zeros(0, np.int64)
+        local = arr[own == self.rank]
+        codes, _ = b.table.find_or_insert_batch(local) if len(local) else (np.zeros(0), None)
+        self.next = [local[codes == 1]]
+        self.full = bool((codes == 2).any())
+        self.outgoing = [arr[own == r] for r in range(self.world)]
+
+    def absorb(self):
+        b = self.base
+        counts = torch.tensor([len(x) if r != self.rank else 0 for r, x in enumerate(self.outgoing)],
+                              dtype=torch.int64)
+        rc = torch.empty_like(counts)
+        dist.all_to_all_single(rc, counts)
+        send = torch.from_numpy(np.concatenate(
+            [x if r != self.rank else np.zeros((0, self.vlen), np.uint32)
+             for r, x in enumerate(self.outgoing)]).astype(np.int32).reshape(-1, self.vlen))
+        recv = torch.empty((int(rc.sum()), self.vlen), dtype=torch.int32)
+        dist.all_to_all_single(recv, send, output_split_sizes=rc.tolist(),
+                               input_split_sizes=counts.tolist())
+        keys = recv.numpy().astype(np.uint32)
+        if len(keys):
+            codes, _ = b.table.find_or_insert_batch(keys)
+            self.next.append(keys[codes == 1])
+            self.full |= bool((codes == 2).any())
+        self.front = np.concatenate(self.next).reshape(-1, self.vlen)
+        self.states += len(self.front)
+        st = np.zeros(8, np.uint64)
+        st[0], st[1], st[2], st[3], st[4] = self.claims, len(self.front), self.trans, self.dl_total, \
+            int(self.full)
+        return st
+
+    def finish(self):
+        class Rep:
+            pass
+        r = Rep()
+        r.states, r.transitions, r.expanded = self.states, self.trans, self.expanded
+        r.deadlocks_total, r.probes = self.dl_total, 0
+        return r, sorted(self.kept)[:100]
+
+
+def _fused_worker(rank, world, port, jobs, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1801_05857_b200.distributed import explore_fused
+    out = []
+    for name, table_kw, max_it in jobs:
+        s = OracleFusedShard(model_path(name), table_kw, world, rank)
+        r = explore_fused(s, dist, torch, True, max_iterations=max_it, device=torch.device("cpu"))
+        out.append((name, r.states, r.transitions, r.iterations, r.deadlocks_total,
+                    tuple(map(tuple, r.deadlocks)), r.outcome, r.expanded))
+    if rank == 0:
+        q.put(out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_fused_driver_matches_single_process():
+    """explore_fused's barrier / reduction / termination logic, world 2
+    and 3 over gloo, against the single-process reference engine."""
+    from oracle import oracle as O
+    names = ["fig1", "ring6", "gas5", "phil4", "sinks8", "collide"]
+    jobs = [(n, {"capacity_words": 1 << 16}, None) for n in names] + \
+        [("ring5", {"capacity_words": 1 << 14}, 3)]
+    models = golden_models()
+    for world in (2, 3):
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=_fused_worker, args=(r, world, port, jobs, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        res = q.get(timeout=600)
+        for p in procs:
+            p.join(timeout=120)
+            assert p.exitcode == 0
+        for (name, states, trans, iters, dl_total, dls, outcome, expanded), job in zip(res, jobs):
+            ref = O.explore(O.Net.from_file(model_path(name)), capacity_words=job[1]["capacity_words"],
+                            detect_deadlocks=True, max_iterations=job[2])
+            assert (states, trans, iters, dl_total, outcome, expanded) == \
+                (ref.states, ref.transitions, ref.iterations, ref.deadlocks_total, ref.outcome,
+                 ref.expanded), (name, world)
+            if job[2] is None:
+                assert sorted(map(list, dls)) == sorted(models[name]["bfs"]["deadlocks"])[:100], name
