@@ -296,13 +296,26 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # more ranks than GPUs (a functional check of the multi-process path on a
+    # one-GPU box): ranks share cuda:0 and the counters go over gloo, since
+    # NCCL refuses two ranks on one device; the inbox IPC mappings are the
+    # same calls
+    oversub = world > 1 and torch.cuda.device_count() < world
+    if oversub:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_1801_05857_b200.distributed import bench_sharded
         line = bench_sharded(args, torch, dist, model_path, closed_form, table_capacity,
                              ClockSampler(local))
+        if oversub:
+            line["config"]["oversubscribed"] = (f"{world} ranks on {torch.cuda.device_count()} GPU(s); "
+                                                "gloo counters")
         if rank == 0:
             print(json.dumps(line), flush=True)
         dist.destroy_process_group()
