@@ -30,9 +30,9 @@ namespace gx {
 
 template <int BW, int V, int G, bool MARK>
 __global__ void __launch_bounds__(256, GX_LEVEL_MINB) k_level(TableDesc T, NetDesc N, LevelArgs A) {
-    constexpr int QCAP = QWORDS / V;
-    __shared__ __align__(16) uint32_t qbuf[8][QWORDS];
-    __shared__ __align__(16) uint32_t obuf[8][QWORDS];
+    constexpr int QCAP = QWORDS_REG / V;
+    __shared__ __align__(16) uint32_t qbuf[8][QWORDS_REG];
+    __shared__ __align__(16) uint32_t obuf[8][QWORDS_REG];
     extern __shared__ unsigned long long dcache[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
@@ -613,6 +613,77 @@ __global__ void __launch_bounds__(256) k_bench(TableDesc T, BenchArgs B) {
 
 typedef void (*bench_kernel_t)(TableDesc, BenchArgs);
 
+// The same benchmark on the staged probe (the level kernel's FINDORPUT):
+// each warp generates KB keys into its shared-memory queue and resolves
+// them with probe_staged.  Counts INSERTED / TABLE_FULL.
+template <int BW, int V>
+__global__ void __launch_bounds__(256, 2) k_bench_staged(TableDesc T, BenchArgs B) {
+    using S = Staged<BW, V>;
+    constexpr int KB = S::KB;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * (KB * V);
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + 8ull * KB * V * 4) + wid * KB;
+    uint4* stage = reinterpret_cast<uint4*>(smem + 8ull * KB * V * 4 + 8ull * KB * 8 +
+                                            (size_t)wid * S::STAGE_BYTES);
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    unsigned long long ins = 0, full = 0;
+    for (uint64_t base = warp * KB; base < B.total; base += nwarps * KB) {
+        const uint32_t m = (uint32_t)min((uint64_t)KB, B.total - base);
+        for (uint32_t k = lane; k < m; k += 32) {
+            uint32_t key[V];
+            bench_key<V>(B, base + k, key);
+#pragma unroll
+            for (int w = 0; w < V; w++) q[k * V + w] = key[w];
+        }
+        __syncwarp();
+        uint32_t f = 0;
+        const uint32_t n_ins = probe_staged<BW, V>(T, q, m, stage, sbkt, &f);
+        ins += lane == 0 ? n_ins : 0;
+        full += f;  // keys that hit TABLE_FULL
+        __syncwarp();
+    }
+    ins = warp_sum(ins);
+    full = warp_sum(full);
+    if (lane == 0) {
+        if (ins) atomicAdd(&B.ctr[0], ins);
+        if (full) atomicAdd(&B.ctr[1], full);
+    }
+}
+
+template <int BW, int V>
+static size_t bench_staged_smem() {
+    using S = Staged<BW, V>;
+    return 8ull * S::KB * V * 4 + 8ull * S::KB * 8 + 8ull * S::STAGE_BYTES;
+}
+
+struct BenchKernel {
+    void (*fn)(TableDesc, BenchArgs);
+    size_t smem;
+};
+
+template <int BW>
+static BenchKernel pick_bench_staged_v(int v) {
+    switch (v) {
+        case 1: return {k_bench_staged<BW, 1>, bench_staged_smem<BW, 1>()};
+        case 2: return {k_bench_staged<BW, 2>, bench_staged_smem<BW, 2>()};
+        case 4: return {k_bench_staged<BW, 4>, bench_staged_smem<BW, 4>()};
+    }
+    return {nullptr, 0};
+}
+
+static BenchKernel pick_bench_staged(const TableDesc& T) {
+    switch (T.bw) {
+        case 4: return pick_bench_staged_v<4>((int)T.vlen);
+        case 8: return pick_bench_staged_v<8>((int)T.vlen);
+        case 16: return pick_bench_staged_v<16>((int)T.vlen);
+        case 32: return pick_bench_staged_v<32>((int)T.vlen);
+    }
+    return {nullptr, 0};
+}
+
 template <int BW, int V>
 static bench_kernel_t pick_bench_g(int g) {
     switch (g) {
@@ -835,7 +906,7 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
     uint32_t cslots = 0;
     if (cfg->cache_slots > 0 && T.mode == MODE_MARK && v <= 2) {
         const size_t budget = 113 * 1024;  // dynamic smem per block at 2 blocks / SM
-        const size_t fixed = LK.fixed_smem + (staged ? 0 : 2 * 8 * QWORDS * 4);
+        const size_t fixed = LK.fixed_smem + (staged ? 0 : 2 * 8 * QWORDS_REG * 4);
         cslots = 1;
         while (cslots * 2 <= (uint32_t)cfg->cache_slots && cslots * 2 <= GX_CACHE_MAX_SLOTS &&
                fixed + 8 * (size_t)cslots * 2 <= budget)
@@ -853,7 +924,9 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
         size_t fr = 0, tot = 0;
         GX_CUDA(cudaMemGetInfo(&fr, &tot));
         const uint64_t reserve = 512ull << 20;
-        uint64_t avail = fr > reserve + t->aux2.bytes ? fr - reserve + t->aux2.bytes : (64ull << 20);
+        // the buffer we already hold counts as available (it is reused)
+        const uint64_t have = (uint64_t)fr + t->aux2.bytes;
+        const uint64_t avail = have > reserve + (64ull << 20) ? have - reserve : (64ull << 20);
         C = std::min<uint64_t>(t->total_slots + 2, avail * 9 / 10 / (4ull * v));
         if (C < 1024) C = 1024;
     }
@@ -1152,7 +1225,10 @@ int gx_bench_find_or_put_rows(gx_table* t, uint64_t total, uint64_t dup, uint64_
         set_error("%llu unique one-word keys do not fit in %d bits", (unsigned long long)unique, key_bits);
         return GX_EINPUT;
     }
-    bench_kernel_t k = pick_bench(T, group);
+    // group 0 (auto) on in-band tables: the staged probe of the level kernel
+    BenchKernel BK = (T.mode == MODE_MARK && group == 0) ? pick_bench_staged(T)
+                                                          : BenchKernel{pick_bench(T, group), 0};
+    bench_kernel_t k = BK.fn;
     if (!k) {
         set_error("no benchmark kernel for bw=%u vlen=%u group=%d", T.bw, T.vlen, group);
         return GX_EINPUT;
@@ -1175,7 +1251,9 @@ int gx_bench_find_or_put_rows(gx_table* t, uint64_t total, uint64_t dup, uint64_
     GX_CUDA(cudaEventCreate(&e0));
     GX_CUDA(cudaEventCreate(&e1));
     GX_CUDA(cudaEventRecord(e0, st));
-    k<<<persistent_grid(), 256, 0, st>>>(T, B);
+    if (BK.smem) GX_CUDA(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)BK.smem));
+    k<<<persistent_grid(), 256, BK.smem, st>>>(T, B);
     GX_LAUNCHED();
     GX_CUDA(cudaEventRecord(e1, st));
     unsigned long long h[2];

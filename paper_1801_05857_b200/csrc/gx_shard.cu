@@ -65,9 +65,9 @@ __global__ void __launch_bounds__(256, 2) k_absorb(TableDesc T, LevelArgs A, con
         uint32_t m = m0;
         if (cmask) m = cache_filter<V>(T, dcache, cmask, q, m);
         probes += lane == 0 ? m : 0;
-        bool full = false;
+        uint32_t full = 0;
         const uint32_t n_out = probe_staged<BW, V>(T, q, m, stage, sbkt, &full);
-        if (__any_sync(FULLMASK, full) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
+        if (__any_sync(FULLMASK, full != 0u) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
         if (n_out) flush_out<V>(A, q, n_out);
         __syncwarp();
     }

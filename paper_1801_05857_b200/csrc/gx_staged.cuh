@@ -17,8 +17,10 @@
 //      are a bucket prefix, hashtable.py:229-231); none -> bucket full
 //   4. all candidates' CASes are issued back to back, then judged: lost to
 //      the same key -> FOUND, lost to another -> walk the rest of the
-//      bucket from global memory; full first bucket -> hash functions
-//      1..K-1 one lane per key (probe_lane; rare below the load cliff)
+//      bucket from global memory (rare)
+//   5. keys whose bucket was full repeat 2-4 with the next hash function,
+//      again all staged at once (hashtable.py:237-280); after K full
+//      buckets -> TABLE_FULL
 //
 // Slot j of a bucket sits at word j*V for every layout the in-band mode
 // allows (vlen 1/2/4: the half layout's second half starts at bw/2, which
@@ -122,104 +124,124 @@ struct Staged {
 // FINDORPUT of keys q[0, m) (V words each, shared memory), KB at a time.
 // INSERTED keys are written back, compacted, to the front of q (a key is
 // only ever written at or below the position it was read from); returns
-// their number.  *full is set if any key hit TABLE_FULL.  stage: this
+// their number.  *full counts (per lane) the keys that hit TABLE_FULL.  stage: this
 // warp's STAGE_BYTES of shared memory; sbkt: its KB bucket indices.
 template <int BW, int V>
 __device__ __forceinline__ uint32_t probe_staged(const TableDesc& T, uint32_t* q, uint32_t m,
                                                  uint4* stage, unsigned long long* sbkt,
-                                                 bool* full) {
+                                                 uint32_t* full) {
     using S = Staged<BW, V>;
     constexpr int KB = S::KB, KPL = S::KPL, CH = S::CH, SPC = S::SPC;
+    constexpr unsigned long long SKIP = ~0ull;
     const int lane = threadIdx.x & 31;
     uint32_t n_ins = 0;
     for (uint32_t r0 = 0; r0 < m; r0 += KB) {
         const uint32_t nb = min((uint32_t)KB, m - r0);
         uint32_t km[KPL][V];
         uint64_t h[KPL], bkt[KPL];
-        bool act[KPL];
+        bool act[KPL], pend[KPL];
+        int rc[KPL];
 #pragma unroll
         for (int i = 0; i < KPL; i++) {
             const uint32_t k = lane + 32 * i;
             act[i] = k < nb;
+            pend[i] = act[i];
+            rc[i] = -1;
             uint32_t key[V];
 #pragma unroll
             for (int w = 0; w < V; w++) key[w] = act[i] ? q[(r0 + k) * V + w] : 0u;
             h[i] = fold<V>(T.salt, key);
-            bkt[i] = act[i] ? bucket_of(T, h[i], 0) : 0;
 #pragma unroll
             for (int w = 0; w < V; w++) km[i][w] = key[w] | (w == (int)T.mark_word ? T.mark : 0u);
-            sbkt[k] = bkt[i];
         }
-        __syncwarp();
-        // stage the first buckets: chunk c = key c / CH, part c % CH
+        // hash function hi for every key still unresolved (hi = 0: all of
+        // them; later rounds only the keys whose bucket was full), each
+        // round with all of its bucket loads in flight at once
+        for (int hi = 0; hi < (int)T.k; hi++) {
+            bool any = false;
 #pragma unroll
-        for (int it = 0; it < KPL * CH; it++) {
-            const uint32_t c = it * 32 + lane;
-            const uint32_t k = c / CH, j = c % CH;
-            if (k < nb)
-                cp_async16(stage + k * CH + (j ^ (k & (CH - 1))),
-                           T.data + sbkt[k] * (uint64_t)BW + 4 * j);
-        }
-        cp_async_wait_all();
-        __syncwarp();
-        // walk each owned bucket from shared memory
-        int slot[KPL], rc[KPL];
-        uint32_t old[KPL][V];
+            for (int i = 0; i < KPL; i++) {
+                const uint32_t k = lane + 32 * i;
+                bkt[i] = pend[i] ? bucket_of(T, h[i], hi) : 0;
+                sbkt[k] = pend[i] ? bkt[i] : SKIP;
+                any |= pend[i];
+            }
+            if (!__any_sync(FULLMASK, any)) break;
+            __syncwarp();
+            // stage the buckets: chunk c = key c / CH, part c % CH
 #pragma unroll
-        for (int i = 0; i < KPL; i++) {
-            const uint32_t k = lane + 32 * i;
-            slot[i] = -1;
-            rc[i] = -1;  // -1: bucket full, try the next hash function
-            if (!act[i]) continue;
-            for (int j = 0; j < CH && rc[i] == -1; j++) {
-                const uint4 c4 = stage[k * CH + (j ^ (k & (CH - 1)))];
-                const uint32_t w4[4] = {c4.x, c4.y, c4.z, c4.w};
+            for (int it = 0; it < KPL * CH; it++) {
+                const uint32_t c = it * 32 + lane;
+                const uint32_t k = c / CH, j = c % CH;
+                const unsigned long long b = sbkt[k];
+                if (b != SKIP)
+                    cp_async16(stage + k * CH + (j ^ (k & (CH - 1))), T.data + b * (uint64_t)BW + 4 * j);
+            }
+            cp_async_wait_all();
+            __syncwarp();
+            // walk each pending bucket from shared memory
+            int slot[KPL];
+            uint32_t old[KPL][V];
 #pragma unroll
-                for (int t = 0; t < SPC; t++) {
-                    if (rc[i] != -1) break;
+            for (int i = 0; i < KPL; i++) {
+                const uint32_t k = lane + 32 * i;
+                slot[i] = -1;
+                if (!pend[i]) continue;
+                for (int j = 0; j < CH && rc[i] == -1; j++) {
+                    const uint4 c4 = stage[k * CH + (j ^ (k & (CH - 1)))];
+                    const uint32_t w4[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+                    for (int t = 0; t < SPC; t++) {
+                        if (rc[i] != -1) break;
+                        bool zero = true, eq = true;
+#pragma unroll
+                        for (int w = 0; w < V; w++) {
+                            zero = zero && w4[t * V + w] == 0u;
+                            eq = eq && w4[t * V + w] == km[i][w];
+                        }
+                        if (eq) {
+                            rc[i] = FOUND;
+                            slot[i] = j * SPC + t;
+                        } else if (zero) {
+                            rc[i] = -3;  // CAS candidate
+                            slot[i] = j * SPC + t;
+                        }
+                    }
+                }
+            }
+            __syncwarp();  // stage and sbkt are free again
+            // the candidates' CASes back to back
+#pragma unroll
+            for (int i = 0; i < KPL; i++)
+                if (pend[i] && rc[i] == -3)
+                    SlotCas<V>::cas(T.data + bkt[i] * (uint64_t)BW + slot[i] * V, km[i], old[i]);
+#pragma unroll
+            for (int i = 0; i < KPL; i++) {
+                if (!pend[i]) continue;
+                if (rc[i] == -3) {
+                    int64_t hd;
                     bool zero = true, eq = true;
 #pragma unroll
                     for (int w = 0; w < V; w++) {
-                        zero = zero && w4[t * V + w] == 0u;
-                        eq = eq && w4[t * V + w] == km[i][w];
+                        zero = zero && old[i][w] == 0u;
+                        eq = eq && old[i][w] == km[i][w];
                     }
-                    if (eq) {
+                    if (zero)
+                        rc[i] = INSERTED;
+                    else if (eq)
                         rc[i] = FOUND;
-                        slot[i] = j * SPC + t;
-                    } else if (zero) {
-                        rc[i] = -3;  // CAS candidate
-                        slot[i] = j * SPC + t;
-                    }
+                    else  // lost the slot to another key: the rest of the bucket
+                        rc[i] = resolve_lane_from<BW, V>(T, bkt[i], slot[i] + 1, km[i], &hd);
                 }
+                pend[i] = rc[i] == -1;  // bucket full: next hash function
             }
         }
-        __syncwarp();  // stage and sbkt are free again
-        // the candidates' CASes back to back
-#pragma unroll
-        for (int i = 0; i < KPL; i++)
-            if (rc[i] == -3)
-                SlotCas<V>::cas(T.data + bkt[i] * (uint64_t)BW + slot[i] * V, km[i], old[i]);
         bool ins[KPL];
 #pragma unroll
         for (int i = 0; i < KPL; i++) {
-            int64_t hd;
-            if (rc[i] == -3) {
-                bool zero = true, eq = true;
-#pragma unroll
-                for (int w = 0; w < V; w++) {
-                    zero = zero && old[i][w] == 0u;
-                    eq = eq && old[i][w] == km[i][w];
-                }
-                if (zero)
-                    rc[i] = INSERTED;
-                else if (eq)
-                    rc[i] = FOUND;
-                else
-                    rc[i] = resolve_lane_from<BW, V>(T, bkt[i], slot[i] + 1, km[i], &hd);
-            }
-            if (act[i] && rc[i] == -1) rc[i] = probe_lane<BW, V>(T, km[i], h[i], 1, &hd);
+            if (act[i] && rc[i] == -1) rc[i] = TABLE_FULL;  // all K buckets full
             ins[i] = act[i] && rc[i] == INSERTED;
-            *full |= act[i] && rc[i] == TABLE_FULL;
+            *full += (act[i] && rc[i] == TABLE_FULL) ? 1u : 0u;
         }
         // INSERTED keys to the front of q, in key order
 #pragma unroll
