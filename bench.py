@@ -433,6 +433,10 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "probes_per_step": rep.probes,
+        "step_breakdown_ms": {"level_kernels": level_ms,
+                              "level_loop": statistics.mean(r.device_ms for r in reps),
+                              "whole_step": ms / args.steps,
+                              "max_frontier": rep.max_frontier},
     }
     if not args.no_hash_bench:
         line["hash_bench"] = {"fill_sweep": hash_sweep(ra), "duplication_sweep": duplication_sweep(ra)}

@@ -77,7 +77,15 @@ typedef struct gx_table_cfg {
     uint64_t seed;              /* hash seed, hashtable.py:50 */
     int32_t mark_word;          /* -1: none */
     int32_t mark_bit;           /* 0..31 */
+    int32_t flags;              /* GX_TABLE_NO_STATUS: see below */
+    int32_t reserved;
 } gx_table_cfg;
+
+/* flags: an in-band (mark bit) table for exploration only, without the
+ * per-slot status array (saves 1 byte per slot, 12.5% of a bw 32 / vlen 2
+ * table).  claim_new / scan_new / dumps / status reads then fail with
+ * GX_EINPUT; explore, find_or_put and occupancy work. */
+#define GX_TABLE_NO_STATUS 1
 
 /* StateTable.__init__ (hashtable.py:137-201).  Allocates and zeroes device
  * memory.  stream: a cudaStream_t or NULL. */
@@ -284,6 +292,12 @@ int gx_bench_find_or_put_rows(gx_table *t, uint64_t total, uint64_t duplication,
  * 8 bytes of every segment read as empty (the FINDORPUT insert path). */
 int gx_random_access_bench(uint64_t buffer_bytes, int32_t granularity, uint64_t reads,
                            int32_t with_cas, int32_t repeats, double *ms_best, double *gbs_best);
+/* Same on a buffer from allocator alloc_kind: 0 cudaMalloc, 1 VMM
+ * (cuMemCreate/cuMemMap at the recommended granularity, returned in
+ * *alloc_granularity), 2 stream-ordered pool (TLB-reach experiments). */
+int gx_random_access_bench_alloc(uint64_t buffer_bytes, int32_t granularity, uint64_t reads,
+                                 int32_t with_cas, int32_t repeats, int32_t alloc_kind,
+                                 double *ms_best, double *gbs_best, uint64_t *alloc_granularity);
 
 /* ----------------------------------------------------------------- misc */
 /* Insertion protocol chosen at create time: 0 = mark bit (single CAS),

@@ -25,7 +25,8 @@ class TableCfg(C.Structure):
     _fields_ = [("bucket_words", C.c_int32), ("num_hash_functions", C.c_int32),
                 ("capacity_words", C.c_uint64), ("layout", C.c_int32),
                 ("vector_length", C.c_int32), ("seed", C.c_uint64),
-                ("mark_word", C.c_int32), ("mark_bit", C.c_int32)]
+                ("mark_word", C.c_int32), ("mark_bit", C.c_int32),
+                ("flags", C.c_int32), ("reserved", C.c_int32)]
 
 
 class NetworkCsr(C.Structure):
@@ -101,6 +102,8 @@ SIGNATURES = {
     "gx_shard_expand": (C.c_int, [_vp]),
     "gx_shard_absorb": (C.c_int, [_vp, _u64p]),
     "gx_shard_finish": (C.c_int, [_vp, _P(Report), _u32p]),
+    "gx_random_access_bench_alloc": (C.c_int, [C.c_uint64, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
+                                               C.c_int32, _P(C.c_double), _P(C.c_double), _u64p]),
     "gx_last_error": (C.c_char_p, []),
     "gx_kernel_launches": (C.c_uint64, []),
     "gx_device_info": (C.c_int, [_i32p, _u64p, _u64p]),

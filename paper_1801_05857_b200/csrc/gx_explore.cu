@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256, GX_LEVEL_MINB) k_level(TableDesc T, NetDe
 }
 
 template <int BW, int V>
-__global__ void __launch_bounds__(256, 2) k_level_staged(TableDesc T, NetDesc N, LevelArgs A) {
+__global__ void __launch_bounds__(256, GX_STAGED_MINB) k_level_staged(TableDesc T, NetDesc N, LevelArgs A) {
     level_staged_body<BW, V, false>(T, N, A, RouteArgs{});
 }
 
@@ -905,7 +905,7 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
     // (only for in-band tables with vlen <= 2)
     uint32_t cslots = 0;
     if (cfg->cache_slots > 0 && T.mode == MODE_MARK && v <= 2) {
-        const size_t budget = 113 * 1024;  // dynamic smem per block at 2 blocks / SM
+        const size_t budget = STAGED_SMEM_BUDGET;
         const size_t fixed = LK.fixed_smem + (staged ? 0 : 2 * 8 * QWORDS_REG * 4);
         cslots = 1;
         while (cslots * 2 <= (uint32_t)cfg->cache_slots && cslots * 2 <= GX_CACHE_MAX_SLOTS &&

@@ -76,6 +76,11 @@ __device__ __forceinline__ void store_state(uint32_t* p, const uint32_t* s) {
 
 // words of shared memory per warp for the successor queue, and the same
 // again for the queue of freshly inserted keys (next-frontier staging)
+#ifndef GX_STAGED_MINB
+#define GX_STAGED_MINB 3  // resident blocks per SM the staged kernels are built for (B200 sweep: 3 > 2)
+#endif
+// dynamic shared memory one block may take so that GX_STAGED_MINB fit per SM
+constexpr size_t STAGED_SMEM_BUDGET = (228 * 1024) / GX_STAGED_MINB - 1024 - 1024;
 #ifndef GX_QWORDS
 #define GX_QWORDS 1024  // B200 sweep (ring16): 512 -> 1024 words cut level time 17%
 #endif

@@ -4,6 +4,8 @@
 // with a 64-bit CAS on every access (the FINDORPUT insert path).  This is
 // the denominator the hash-table probes are judged against: a probe can
 // never beat the rate at which HBM serves random g-byte segments.
+#include <cuda.h>
+
 #include "gx_internal.h"
 
 namespace gx {
@@ -64,9 +66,109 @@ static rr_kernel_t pick_rr(int g) {
 
 using namespace gx;
 
+extern "C" int gx_random_access_bench_alloc(uint64_t, int32_t, uint64_t, int32_t, int32_t, int32_t,
+                                            double*, double*, uint64_t*);
+
+// Driver-API entry points resolved through the runtime (no link-time
+// dependency on libcuda, so the library still loads on a CPU-only host).
+struct DrvVmm {
+    CUresult (*granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags);
+    CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+    CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+    CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+    CUresult (*access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+    CUresult (*unmap)(CUdeviceptr, size_t);
+    CUresult (*release)(CUmemGenericAllocationHandle);
+    CUresult (*addr_free)(CUdeviceptr, size_t);
+};
+
+static bool drv_vmm(DrvVmm* d) {
+    cudaDriverEntryPointQueryResult q;
+    const char* names[8] = {"cuMemGetAllocationGranularity", "cuMemAddressReserve", "cuMemCreate", "cuMemMap",
+                            "cuMemSetAccess", "cuMemUnmap", "cuMemRelease", "cuMemAddressFree"};
+    void** slots[8] = {(void**)&d->granularity, (void**)&d->reserve, (void**)&d->create, (void**)&d->map,
+                       (void**)&d->access, (void**)&d->unmap, (void**)&d->release, (void**)&d->addr_free};
+    for (int i = 0; i < 8; i++)
+        if (cudaGetDriverEntryPoint(names[i], slots[i], cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+    return true;
+}
+
+// Device buffer for the benchmark: 0 = cudaMalloc, 1 = VMM (cuMemCreate +
+// cuMemMap at the recommended granularity), 2 = stream-ordered pool.
+static int rr_alloc(int kind, uint64_t bytes, void** p, uint64_t* gran, CUmemGenericAllocationHandle* h) {
+    *gran = 0;
+    if (kind == 1) {
+        DrvVmm D;
+        if (!drv_vmm(&D)) {
+            set_error("driver VMM entry points unavailable");
+            return GX_EINTERNAL;
+        }
+        int dev = 0;
+        GX_CUDA(cudaGetDevice(&dev));
+        CUmemAllocationProp prop = {};
+        prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        prop.location.id = dev;
+        size_t g = 0;
+        if (D.granularity(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS) {
+            set_error("cuMemGetAllocationGranularity failed");
+            return GX_EINTERNAL;
+        }
+        *gran = g;
+        bytes = (bytes + g - 1) / g * g;
+        CUdeviceptr va = 0;
+        if (D.reserve(&va, bytes, g, 0, 0) != CUDA_SUCCESS || D.create(h, bytes, &prop, 0) != CUDA_SUCCESS ||
+            D.map(va, bytes, 0, *h, 0) != CUDA_SUCCESS) {
+            set_error("VMM allocation failed");
+            return GX_EINTERNAL;
+        }
+        CUmemAccessDesc acc = {};
+        acc.location = prop.location;
+        acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        if (D.access(va, bytes, &acc, 1) != CUDA_SUCCESS) {
+            set_error("cuMemSetAccess failed");
+            return GX_EINTERNAL;
+        }
+        *p = (void*)va;
+        return GX_OK;
+    }
+    if (kind == 2) {
+        GX_CUDA(cudaMallocAsync(p, bytes, 0));
+        GX_CUDA(cudaStreamSynchronize(0));
+        return GX_OK;
+    }
+    GX_CUDA(cudaMalloc(p, bytes));
+    return GX_OK;
+}
+
+static void rr_free(int kind, void* p, uint64_t bytes, uint64_t gran, CUmemGenericAllocationHandle h) {
+    if (kind == 1) {
+        DrvVmm D;
+        if (!drv_vmm(&D)) return;
+        bytes = (bytes + gran - 1) / gran * gran;
+        D.unmap((CUdeviceptr)p, bytes);
+        D.release(h);
+        D.addr_free((CUdeviceptr)p, bytes);
+    } else if (kind == 2) {
+        cudaFreeAsync(p, 0);
+        cudaStreamSynchronize(0);
+    } else {
+        cudaFree(p);
+    }
+}
+
 extern "C" int gx_random_access_bench(uint64_t buffer_bytes, int32_t granularity, uint64_t reads,
                                       int32_t with_cas, int32_t repeats, double* ms_best,
                                       double* gbs_best) {
+    return gx_random_access_bench_alloc(buffer_bytes, granularity, reads, with_cas, repeats, 0, ms_best,
+                                        gbs_best, nullptr);
+}
+
+extern "C" int gx_random_access_bench_alloc(uint64_t buffer_bytes, int32_t granularity, uint64_t reads,
+                                            int32_t with_cas, int32_t repeats, int32_t alloc_kind,
+                                            double* ms_best, double* gbs_best, uint64_t* alloc_granularity) {
     rr_kernel_t k = with_cas ? pick_rr<true>(granularity) : pick_rr<false>(granularity);
     if (!k || buffer_bytes < (uint64_t)granularity || reads == 0 || repeats < 1) {
         set_error("random_access_bench: granularity must be 16/32/64/128 and sizes positive");
@@ -74,7 +176,11 @@ extern "C" int gx_random_access_bench(uint64_t buffer_bytes, int32_t granularity
     }
     void* buf = nullptr;
     unsigned long long* sink = nullptr;
-    GX_CUDA(cudaMalloc(&buf, buffer_bytes));
+    uint64_t gran = 0;
+    CUmemGenericAllocationHandle vh = 0;
+    int rc = rr_alloc(alloc_kind, buffer_bytes, &buf, &gran, &vh);
+    if (rc) return rc;
+    if (alloc_granularity) *alloc_granularity = gran;
     GX_CUDA(cudaMalloc(&sink, 8));
     GX_CUDA(cudaMemset(buf, 0, buffer_bytes));
     const uint64_t segments = buffer_bytes / granularity;
@@ -95,7 +201,7 @@ extern "C" int gx_random_access_bench(uint64_t buffer_bytes, int32_t granularity
     }
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    cudaFree(buf);
+    rr_free(alloc_kind, buf, buffer_bytes, gran, vh);
     cudaFree(sink);
     *ms_best = best;
     *gbs_best = (double)reads * granularity / (best * 1e-3) / 1e9;

@@ -30,14 +30,14 @@
 namespace gx {
 
 template <int BW, int V>
-__global__ void __launch_bounds__(256, 2) k_level_routed(TableDesc T, NetDesc N, LevelArgs A, RouteArgs R) {
+__global__ void __launch_bounds__(256, GX_STAGED_MINB) k_level_routed(TableDesc T, NetDesc N, LevelArgs A, RouteArgs R) {
     level_staged_body<BW, V, true>(T, N, A, R);
 }
 
 // FINDORPUT the inbox (n = *count keys, clamped to cap); inserted keys go to
 // the next frontier through the level's LevelArgs.
 template <int BW, int V>
-__global__ void __launch_bounds__(256, 2) k_absorb(TableDesc T, LevelArgs A, const uint32_t* __restrict__ inbox,
+__global__ void __launch_bounds__(256, GX_STAGED_MINB) k_absorb(TableDesc T, LevelArgs A, const uint32_t* __restrict__ inbox,
                                                   const unsigned long long* count, uint64_t cap) {
     using L = StagedSmem<BW, V>;
     using S = Staged<BW, V>;
@@ -174,7 +174,7 @@ int gx_shard_create(gx_net* n, gx_table* t, int32_t rank, int32_t world, uint64_
     s->K = K;
     s->cslots = 0;
     if (cache_slots > 0 && T.vlen <= 2) {
-        const size_t budget = 113 * 1024;
+        const size_t budget = STAGED_SMEM_BUDGET;
         uint32_t c = 1;
         while (c * 2 <= (uint32_t)cache_slots && c * 2 <= GX_CACHE_MAX_SLOTS && K.fixed_smem + 16 * (size_t)c <= budget)
             c *= 2;

@@ -32,7 +32,7 @@
 #define GX_STAGE_BYTES 8192  // shared-memory bucket staging per warp
 #endif
 #ifndef GX_STAGE_KB_MAX
-#define GX_STAGE_KB_MAX 64  // keys per staged batch at most (B200 sweep: 64 ~ 128 > 256)
+#define GX_STAGE_KB_MAX 32  // keys per staged batch at most (B200 sweeps: 3 blocks x 32 > 2 blocks x 64)
 #endif
 
 namespace gx {

@@ -338,6 +338,10 @@ __global__ void __launch_bounds__(256) k_select_write(TableDesc T, uint64_t firs
 
 static int select_slots(gx_table* t, uint64_t first, uint64_t last, int pred, int64_t* h_out,
                         uint8_t* s_out, uint32_t* w_out, uint64_t cap, uint64_t* count) {
+    if (!t->d.status) {
+        set_error("table was created without a status array (GX_TABLE_NO_STATUS)");
+        return GX_EINPUT;
+    }
     const TableDesc& T = t->d;
     if (last > T.nb) last = T.nb;
     if (first >= last) {
@@ -427,6 +431,7 @@ __global__ void k_mark_new(TableDesc T, const int64_t* __restrict__ handles, uin
 }
 
 int table_fixup_status(gx_table* t, const uint32_t* d_new_keys, uint64_t n_new) {
+    if (!t->d.status) return GX_OK;  // exploration-only table: no statuses to keep
     const TableDesc& T = t->d;
     int grid = (int)std::min<uint64_t>((uint64_t)sm_count() * 8, (T.nb + 255) / 256);
     if (grid < 1) grid = 1;
@@ -564,7 +569,8 @@ int gx_table_create(const gx_table_cfg* cfg, void* stream, gx_table** out) {
     T.salt = splitmix_next(&y);
     t->total_slots = nb * (uint64_t)spb;
     cudaError_t e1 = cudaMalloc(&T.data, nb * (uint64_t)bw * 4);
-    cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&T.status, nb * (uint64_t)T.stride) : e1;
+    const bool no_status = mark_ok && (cfg->flags & GX_TABLE_NO_STATUS);
+    cudaError_t e2 = e1 == cudaSuccess && !no_status ? cudaMalloc(&T.status, nb * (uint64_t)T.stride) : e1;
     cudaError_t e3 = e2 == cudaSuccess ? cudaMalloc(&t->d_ctr, sizeof(uint64_t) * CTR_N) : e2;
     cudaError_t e4 = e3 == cudaSuccess ? cudaMallocHost(&t->h_ctr, sizeof(uint64_t) * CTR_N) : e3;
     if (e4 != cudaSuccess) {
@@ -606,7 +612,7 @@ int gx_table_destroy(gx_table* t) {
 int gx_table_clear(gx_table* t) {
     const TableDesc& T = t->d;
     GX_CUDA(cudaMemsetAsync(T.data, 0, T.nb * (uint64_t)T.bw * 4, t->stream));
-    GX_CUDA(cudaMemsetAsync(T.status, 0, T.nb * (uint64_t)T.stride, t->stream));
+    if (T.status) GX_CUDA(cudaMemsetAsync(T.status, 0, T.nb * (uint64_t)T.stride, t->stream));
     GX_CUDA(cudaMemsetAsync(t->d_ctr, 0, sizeof(uint64_t) * CTR_N, t->stream));
     return GX_OK;
 }
@@ -669,6 +675,10 @@ int gx_find_or_put_device(gx_table* t, const uint32_t* d_keys, uint64_t n, uint8
 }
 
 int gx_claim_new(gx_table* t, const int64_t* handles, uint64_t n, uint8_t* claimed) {
+    if (!t->d.status) {
+        set_error("table was created without a status array (GX_TABLE_NO_STATUS)");
+        return GX_EINPUT;
+    }
     if (n == 0) return GX_OK;
     int rc = t->handles.ensure(sizeof(int64_t) * n);
     if (!rc) rc = t->codes.ensure(n);
@@ -699,6 +709,10 @@ int gx_occupancy(gx_table* t, uint64_t* occupied, uint64_t* new_count) {
 }
 
 int gx_read_slots(gx_table* t, const int64_t* handles, uint64_t n, uint8_t* status, uint32_t* words) {
+    if (status && !t->d.status) {
+        set_error("table was created without a status array (GX_TABLE_NO_STATUS)");
+        return GX_EINPUT;
+    }
     if (n == 0) return GX_OK;
     const uint64_t v = t->d.vlen;
     int rc = t->handles.ensure(sizeof(int64_t) * n);

@@ -154,7 +154,7 @@ class FusedShard:
     its own; after the level barrier each shard absorbs its inbox."""
 
     def __init__(self, net, cfg, rank: int, world: int, inbox_capacity: int = 0,
-                 frontier_capacity: int = 0, stream=None):
+                 frontier_capacity: int = 0, stream=None, status: bool = True):
         from . import statevec
         from ._lib import check, lib
         from .explore import DeviceNetwork
@@ -165,7 +165,7 @@ class FusedShard:
         self.vlen = self.scheme.vector_length
         self.dnet = DeviceNetwork(net, self.scheme, stream)
         self.table = StateTable(cfg.table, self.vlen, mark=statevec.mark_bit(self.scheme),
-                                stream=stream)
+                                stream=stream, status=status)
         slots = self.table.total_slots
         if not frontier_capacity:
             sm, free, _tot = device_info()
@@ -293,7 +293,8 @@ def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None) -> S
     return tot, sorted(kept)[:100], rounds, outcome
 
 
-def explore_local_shards(net, cfg, world: int, inbox_capacity: int = 0, frontier_capacity: int = 0):
+def explore_local_shards(net, cfg, world: int, inbox_capacity: int = 0, frontier_capacity: int = 0,
+                         status: bool = True):
     """Hash-owner sharded exploration with all `world` shards in this
     process (one GPU): the multi-GPU protocol and kernels, with peer
     inboxes as local device memory.  Returns an ExplorationReport; its
@@ -302,7 +303,8 @@ def explore_local_shards(net, cfg, world: int, inbox_capacity: int = 0, frontier
 
     from .explore import ExplorationReport
 
-    shards = [FusedShard(net, cfg, r, world, inbox_capacity, frontier_capacity) for r in range(world)]
+    shards = [FusedShard(net, cfg, r, world, inbox_capacity, frontier_capacity, status=status)
+              for r in range(world)]
     try:
         connect_local(shards)
         t0 = time.perf_counter()

@@ -156,13 +156,13 @@ class Explorer:
     """Reusable device explorer: network CSR + state table stay resident
     across runs (the table is cleared at the start of every run)."""
 
-    def __init__(self, net: Network, cfg: ExploreConfig, stream=None):
+    def __init__(self, net: Network, cfg: ExploreConfig, stream=None, status: bool = True):
         self.net = net
         self.cfg = cfg
         self.scheme = statevec.make_scheme(net)
         self.dnet = DeviceNetwork(net, self.scheme, stream)
         self.table = StateTable(cfg.table, self.scheme.vector_length,
-                                mark=statevec.mark_bit(self.scheme), stream=stream)
+                                mark=statevec.mark_bit(self.scheme), stream=stream, status=status)
         self.last = None
 
     def run(self) -> ExplorationReport:

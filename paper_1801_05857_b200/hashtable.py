@@ -96,9 +96,13 @@ class StateTable:
     the packing scheme); the table then inserts with one CAS per key and
     probes only data sectors.  Without it every key pattern is allowed and
     the claim/publish status protocol of the reference is used.
+    `status=False` (in-band tables only) drops the per-slot status array
+    for exploration-only tables: 12.5% less memory at bw 32 / vlen 2; the
+    claim / scan / dump methods then raise ValueError.
     """
 
-    def __init__(self, config: TableConfig, vector_length: int, mark=None, stream=None):
+    def __init__(self, config: TableConfig, vector_length: int, mark=None, stream=None,
+                 status: bool = True):
         if config.bucket_words not in BUCKET_WORD_CHOICES:
             raise ValueError(f"bucket_words must be one of {BUCKET_WORD_CHOICES}, "
                              f"got {config.bucket_words}")
@@ -121,7 +125,8 @@ class StateTable:
         self._fold_salt = next(_splitmix((config.seed ^ 0xA5A5A5A5A5A5A5A5) & MASK64))
         cfg = TableCfg(config.bucket_words, config.num_hash_functions, config.capacity_words,
                        1 if layout == HALF_BUCKET else 0, vector_length, config.seed & MASK64,
-                       mark[0] if mark else -1, mark[1] if mark else 0)
+                       mark[0] if mark else -1, mark[1] if mark else 0,
+                       0 if status else 1, 0)  # GX_TABLE_NO_STATUS: exploration-only table
         h = C.c_void_p()
         check(lib().gx_table_create(C.byref(cfg), stream, C.byref(h)))
         self._h = h
