@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--probe-group", type=int, default=0)
     ap.add_argument("--cache-slots", type=int, default=4096,
                     help="per-block shared-memory dedup cache entries (< 32 = off)")
+    ap.add_argument("--filter-log2", type=int, default=0,
+                    help="GPU-wide L2 dedup filter of 2^k entries (0 = off)")
     ap.add_argument("--cpu-sample", default="ring12")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hash-bench", action="store_true",
@@ -341,7 +343,7 @@ def main():
     tcfg = TableConfig(bucket_words=args.bucket_words, num_hash_functions=args.hash_functions,
                        capacity_words=cap)
     cfg = ExploreConfig(table=tcfg, detect_deadlocks=True, probe_group=args.probe_group,
-                        cache_slots=max(1, args.cache_slots))
+                        cache_slots=max(1, args.cache_slots), filter_log2=args.filter_log2)
     stream = torch.cuda.current_stream().cuda_stream
     ex = Explorer(net, cfg, stream=stream)
     table_bytes = ex.table.num_buckets * (4 * args.bucket_words + ((ex.table.slots_per_bucket + 7) & ~7))
@@ -413,7 +415,7 @@ def main():
             "states": rep.states, "transitions": rep.transitions, "levels": rep.iterations - 1,
             "vector_words": vlen, "bucket_words": args.bucket_words,
             "hash_functions": args.hash_functions, "table_bytes": table_bytes,
-            "block_cache_slots": args.cache_slots,
+            "block_cache_slots": args.cache_slots, "l2_filter_log2": args.filter_log2,
             "load_factor": rep.states / ex.table.total_slots,
             "l2_policy": "table re-zeroed every step; table >> 126 MB L2",
             "parallelism": "single GPU",

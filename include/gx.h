@@ -172,7 +172,8 @@ int gx_expand(gx_net *n, const uint32_t *states, uint64_t nstates, uint64_t *cou
 /* ExploreConfig (explore.py:47-62) minus the CPU worker knobs. */
 typedef struct gx_explore_cfg {
     int32_t detect_deadlocks;
-    int32_t reserved0;
+    int32_t filter_log2;        /* > 0: GPU-wide L2-resident dedup filter of 2^filter_log2
+                                   entries (8 B each) in front of the table; 0 = off */
     int64_t max_iterations;     /* <= 0: none */
     uint64_t frontier_capacity; /* vectors; 0 = size from free device memory */
     int32_t probe_group;        /* 0 = auto; else lanes per bucket probe (1,2,4,8) */
@@ -251,7 +252,8 @@ typedef struct gx_shard gx_shard;
 #define GX_SH_PROBES 7
 #define GX_SH_N 8
 int gx_shard_create(gx_net *n, gx_table *t, int32_t rank, int32_t world, uint64_t inbox_capacity,
-                    uint64_t frontier_capacity, int32_t cache_slots, gx_shard **out);
+                    uint64_t frontier_capacity, int32_t cache_slots, int32_t filter_log2,
+                    gx_shard **out);
 int gx_shard_destroy(gx_shard *s);
 /* CUDA IPC handle of this shard's inbox (GX_IPC_HANDLE_BYTES bytes) */
 int gx_shard_ipc_handle(gx_shard *s, uint8_t *out);

@@ -38,7 +38,7 @@ class NetworkCsr(C.Structure):
 
 
 class ExploreCfg(C.Structure):
-    _fields_ = [("detect_deadlocks", C.c_int32), ("reserved0", C.c_int32),
+    _fields_ = [("detect_deadlocks", C.c_int32), ("filter_log2", C.c_int32),
                 ("max_iterations", C.c_int64), ("frontier_capacity", C.c_uint64),
                 ("probe_group", C.c_int32), ("cache_slots", C.c_int32)]
 
@@ -93,7 +93,7 @@ SIGNATURES = {
     "gx_random_access_bench": (C.c_int, [C.c_uint64, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
                                          _P(C.c_double), _P(C.c_double)]),
     "gx_shard_create": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_uint64, C.c_uint64, C.c_int32,
-                                  _P(_vp)]),
+                                  C.c_int32, _P(_vp)]),
     "gx_shard_destroy": (C.c_int, [_vp]),
     "gx_shard_ipc_handle": (C.c_int, [_vp, _u8p]),
     "gx_shard_connect": (C.c_int, [_vp, _u8p]),

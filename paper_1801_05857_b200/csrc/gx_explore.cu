@@ -918,6 +918,14 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
                                  (int)csmem));
     int rc = gx_table_clear(t);
     if (rc) return rc;
+    // GPU-wide L2 dedup filter (in-band tables, vlen <= 2), cleared per search
+    uint64_t gslots = 0;
+    if (cfg->filter_log2 > 0 && T.mode == MODE_MARK && v <= 2) {
+        gslots = 1ull << std::min(cfg->filter_log2, 28);
+        rc = t->gfilter.ensure(8 * gslots);
+        if (rc) return rc;
+        GX_CUDA(cudaMemsetAsync(t->gfilter.p, 0, 8 * gslots, st));
+    }
     // frontier buffer: two-ended, capacity C vectors
     uint64_t C = cfg->frontier_capacity;
     if (C == 0) {
@@ -990,7 +998,8 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
                 A.dl = (uint32_t*)n->dl.p;
                 A.dl_cap = dl_cap;
                 A.cache_mask = cslots ? cslots - 1 : 0;
-                A.pad = 0;
+                A.gfilter_mask = gslots ? (uint32_t)(gslots - 1) : 0;
+                A.gfilter = (unsigned long long*)t->gfilter.p;
                 const uint64_t want = (nF + 31) / 32;  // warps
                 const int g = (int)std::min<uint64_t>((uint64_t)grid, (want + 7) / 8);
                 GX_CUDA(cudaEventRecord(la, st));

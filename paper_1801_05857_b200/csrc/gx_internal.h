@@ -86,7 +86,7 @@ struct gx_table {
     uint64_t total_slots;
     uint64_t* d_ctr;   // CTR_N cells
     uint64_t* h_ctr;   // pinned mirror
-    gx::DevBuf keys, codes, handles, aux, aux2;
+    gx::DevBuf keys, codes, handles, aux, aux2, gfilter;
 };
 
 struct gx_net {

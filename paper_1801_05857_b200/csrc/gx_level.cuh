@@ -27,7 +27,8 @@ struct LevelArgs {
     uint32_t* dl;
     uint64_t dl_cap;
     uint32_t cache_mask;  // block-local dedup cache slots - 1 (0 = no cache)
-    uint32_t pad;
+    uint32_t gfilter_mask;  // GPU-wide dedup filter slots - 1 (0 = none)
+    unsigned long long* gfilter;
 };
 
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
@@ -140,6 +141,44 @@ __device__ __forceinline__ uint32_t cache_filter(const TableDesc& T, unsigned lo
             const uint64_t h = fold<V>(T.salt, key);
             const unsigned long long kv = cache_word<V>(T, key);
             keep = atomicExch(&cache[(uint32_t)(h ^ (h >> 32)) & cmask], kv) != kv;
+        }
+        const uint32_t km = __ballot_sync(FULLMASK, keep);
+        __syncwarp();
+        if (keep) {
+            const uint32_t p = kept + __popc(km & lanemask_lt());
+#pragma unroll
+            for (int w = 0; w < V; w++) q[p * V + w] = key[w];
+        }
+        kept += __popc(km);
+        __syncwarp();
+    }
+    return kept;
+}
+
+// GPU-wide dedup filter: the same exchange protocol as the block cache on a
+// direct-mapped array small enough to stay in L2 (and inside the TLB's
+// reach), so a successor generated again anywhere on the GPU -- the BFS
+// "diamonds" of independent moves -- skips its random probe of the big
+// table.  Keys are only dropped when the filter already held them, i.e.
+// someone has FINDORPUT (or is FINDORPUTting) them.  The filter is cleared
+// with the table, so it never outlives the keys it vouches for.
+template <int V>
+__device__ __forceinline__ uint32_t global_filter(const TableDesc& T, unsigned long long* gf,
+                                                  uint32_t gmask, uint32_t* q, uint32_t m) {
+    const int lane = threadIdx.x & 31;
+    uint32_t kept = 0;
+    for (uint32_t r0 = 0; r0 < m; r0 += 32) {
+        const uint32_t e = r0 + lane;
+        const bool a = e < m;
+        uint32_t key[V];
+#pragma unroll
+        for (int w = 0; w < V; w++) key[w] = a ? q[e * V + w] : 0u;
+        bool keep = false;
+        if (a) {
+            const uint64_t h = fold<V>(T.salt, key);
+            const unsigned long long kv = cache_word<V>(T, key);
+            const uint32_t idx = (uint32_t)((h * 0xD6E8FEB86659FD93ull) >> 32) & gmask;
+            keep = atomicExch(&gf[idx], kv) != kv;
         }
         const uint32_t km = __ballot_sync(FULLMASK, keep);
         __syncwarp();
@@ -329,6 +368,7 @@ __device__ __forceinline__ void level_staged_body(const TableDesc& T, const NetD
             __syncwarp();
             uint32_t m = c1 - c0;
             if (cmask) m = cache_filter<V>(T, dcache, cmask, q, m);
+            if (V <= 2 && A.gfilter_mask) m = global_filter<V>(T, A.gfilter, A.gfilter_mask, q, m);
             if (ROUTE) m = route_remote<V>(T, R, q, m, &A.ctr[LV_OVF], &routed);
             probes += lane == 0 ? m : 0;
             uint32_t full = 0;

@@ -125,8 +125,9 @@ struct gx_shard {
     RouteArgs R;
     bool connected = false;
     // two-ended frontier buffer
-    DevBuf fb, dl;
+    DevBuf fb, dl, gf;
     uint64_t C;
+    uint64_t gslots = 0;  // GPU-wide dedup filter entries (0 = off)
     const uint32_t* F = nullptr;
     uint64_t nF = 0;
     int rev = 1;
@@ -145,7 +146,8 @@ struct gx_shard {
 extern "C" {
 
 int gx_shard_create(gx_net* n, gx_table* t, int32_t rank, int32_t world, uint64_t inbox_capacity,
-                    uint64_t frontier_capacity, int32_t cache_slots, gx_shard** out) {
+                    uint64_t frontier_capacity, int32_t cache_slots, int32_t filter_log2,
+                    gx_shard** out) {
     *out = nullptr;
     const TableDesc& T = t->d;
     if (world < 1 || world > GX_MAX_SHARDS || rank < 0 || rank >= world) {
@@ -196,6 +198,10 @@ int gx_shard_create(gx_net* n, gx_table* t, int32_t rank, int32_t world, uint64_
     }
     int rc = s->fb.ensure(sizeof(uint32_t) * s->C * T.vlen);
     if (!rc) rc = s->dl.ensure(sizeof(uint32_t) * s->dl_cap * T.vlen);
+    if (!rc && filter_log2 > 0 && T.vlen <= 2) {
+        s->gslots = 1ull << std::min(filter_log2, 28);
+        rc = s->gf.ensure(8 * s->gslots);
+    }
     if (rc) {
         cudaFree(s->inbox_block);
         delete s;
@@ -218,6 +224,7 @@ int gx_shard_destroy(gx_shard* s) {
     cudaFree(s->inbox_block);
     s->fb.release();
     s->dl.release();
+    s->gf.release();
     cudaEventDestroy(s->e0);
     cudaEventDestroy(s->e1);
     cudaEventDestroy(s->e2);
@@ -282,6 +289,7 @@ int gx_shard_begin(gx_shard* s, int32_t owns_initial, int32_t detect_deadlocks, 
     int rc = gx_table_clear(t);
     if (rc) return rc;
     GX_CUDA(cudaMemsetAsync(s->inbox_block, 0, INBOX_HEAD, s->stream));
+    if (s->gslots) GX_CUDA(cudaMemsetAsync(s->gf.p, 0, 8 * s->gslots, s->stream));
     s->F = (const uint32_t*)s->fb.p;
     s->nF = 0;
     s->rev = 1;
@@ -333,12 +341,13 @@ int gx_shard_expand(gx_shard* s) {
     A.dl = (uint32_t*)s->dl.p;
     A.dl_cap = s->dl_cap;
     A.cache_mask = s->cslots ? s->cslots - 1 : 0;
-    A.pad = 0;
+    A.gfilter_mask = s->gslots ? (uint32_t)(s->gslots - 1) : 0;
+    A.gfilter = (unsigned long long*)s->gf.p;
     (void)v;
     GX_CUDA(cudaEventRecord(s->e0, s->stream));
     if (s->nF) {
         const uint64_t want = (s->nF + 31) / 32;
-        const int g = (int)std::min<uint64_t>((uint64_t)sm_count() * 2, (want + 7) / 8);
+        const int g = (int)std::min<uint64_t>((uint64_t)sm_count() * GX_STAGED_MINB, (want + 7) / 8);
         s->K.a<<<g, 256, s->smem, s->stream>>>(t->d, s->n->d, A, s->R);
         GX_LAUNCHED();
     }
@@ -352,7 +361,7 @@ int gx_shard_absorb(gx_shard* s, uint64_t* stats) {
     cudaStream_t st = s->stream;
     // the inbox fill is only known on the device: a persistent grid that
     // exits at once when nothing arrived
-    s->K.b<<<sm_count() * 2, 256, s->smem, st>>>(t->d, s->A, s->R.inbox[s->rank],
+    s->K.b<<<sm_count() * GX_STAGED_MINB, 256, s->smem, st>>>(t->d, s->A, s->R.inbox[s->rank],
                                                  s->R.inbox_ctr[s->rank], s->inbox_cap);
     GX_LAUNCHED();
     GX_CUDA(cudaEventRecord(s->e2, st));

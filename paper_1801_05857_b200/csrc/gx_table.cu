@@ -605,6 +605,7 @@ int gx_table_destroy(gx_table* t) {
     t->handles.release();
     t->aux.release();
     t->aux2.release();
+    t->gfilter.release();
     delete t;
     return GX_OK;
 }

@@ -176,7 +176,7 @@ class FusedShard:
         h = C.c_void_p()
         check(lib().gx_shard_create(self.dnet.handle, self.table.handle, rank, world, inbox_capacity,
                                     frontier_capacity, int(min(cfg.cache_slots, 1 << 30)),
-                                    C.byref(h)))
+                                    int(cfg.filter_log2), C.byref(h)))
         self._h = h
         self.init = np.asarray(statevec.pack(self.scheme, net.initial), np.uint32)
 

@@ -51,6 +51,10 @@ class ExploreConfig:
     # from free HBM) and lanes per bucket probe (0 = one 16-byte chunk each)
     frontier_capacity: int = 0
     probe_group: int = 0
+    # GPU-wide L2-resident dedup filter of 2^filter_log2 entries in front of
+    # the table (0 = off): duplicate successors generated anywhere on the GPU
+    # skip their random table probe
+    filter_log2: int = 0
 
     def __post_init__(self):
         if self.workers < 1:
@@ -167,7 +171,7 @@ class Explorer:
 
     def run(self) -> ExplorationReport:
         cfg = self.cfg
-        ecfg = ExploreCfg(int(cfg.detect_deadlocks), 0, int(cfg.max_iterations or 0),
+        ecfg = ExploreCfg(int(cfg.detect_deadlocks), int(cfg.filter_log2), int(cfg.max_iterations or 0),
                           int(cfg.frontier_capacity), int(cfg.probe_group),
                           int(min(cfg.cache_slots, 1 << 30)))
         rep = Report()

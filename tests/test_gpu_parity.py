@@ -327,3 +327,17 @@ def test_deadlock_keep_smallest():
     from itertools import product
     want = sorted((1,) + bits for bits in product((2, 3), repeat=10))[:100]
     assert [tuple(s) for s in rep.deadlocks] == want
+
+
+def test_cli_explore_json(capsys):
+    """`python -m paper_1801_05857_b200 explore NET --json --deadlock` prints
+    the reference's JSON report (docs/cli.md:28-55) with the golden counts."""
+    from paper_1801_05857_b200.cli import main
+    for name, extra in (("fig1", []), ("sinks8", ["--shards", "2"])):
+        rc = main(["explore", str(model_path(name)), "--json", "--deadlock", "--table-mb", "4", *extra])
+        assert rc == 0
+        doc = json.loads(capsys.readouterr().out)
+        b = MODELS[name]["bfs"]
+        assert (doc["states"], doc["transitions"], doc["deadlocks_total"], doc["outcome"]) == \
+            (b["states"], b["transitions"], b["deadlocks_total"], "COMPLETE")
+        assert doc["config"]["bucket_words"] == 32

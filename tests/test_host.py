@@ -188,3 +188,18 @@ def test_library_loads_and_reports_launch_counter():
     from paper_1801_05857_b200 import _lib
     assert _lib.kernel_launches() >= 0
     assert isinstance(_lib.last_error(), str)
+
+
+# ------------------------------------------------------------------ CLI
+
+def test_cli_gen_model_and_input_errors(tmp_path, capsys):
+    """cli.py mirrors ltsmc's subcommands and exit codes (cli.py:28-31)."""
+    from paper_1801_05857_b200.cli import main
+    assert main(["gen-model", "token-ring", "--n", "3", "--out", str(tmp_path / "r3")]) == 0
+    out = capsys.readouterr().out
+    assert out.startswith("config[gen-model]:") and "net.exp" in out
+    assert (tmp_path / "r3" / "net.exp").exists()
+    assert main(["explore", str(tmp_path / "missing.exp")]) == 1
+    assert main(["explore", str(tmp_path / "r3" / "net.exp"), "--oracle"]) == 1
+    assert main(["explore", "--bucket-size", "5", "x"]) == 1
+    assert main(["nonsense"]) == 1
