@@ -42,6 +42,8 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 PEAKS = ROOT / "MEASURED_PEAKS.json"
+TLB_REACH = 60 << 30    # one table beyond this: shard it on the GPU (profiles/README.md)
+SHARD_BYTES = 40 << 30  # target table bytes per shard
 TRAFFIC = ROOT / "profiles" / "traffic.json"
 METRIC = "states explored/sec"
 
@@ -52,11 +54,19 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
-    ap.add_argument("--workload", default="ring16",
-                    help="ringN | gasN | petersonN (generated models)")
+    ap.add_argument("--workload", default="ring19",
+                    help="ringN | gasN | petersonN (generated models); default ring19 = "
+                         "BASELINE configs[3], a ~157 GB table")
     ap.add_argument("--bucket-words", type=int, default=32)
-    ap.add_argument("--hash-functions", type=int, default=8)
-    ap.add_argument("--load", type=float, default=0.5, help="target table load factor")
+    ap.add_argument("--hash-functions", type=int, default=32,
+                    help="K (the reference default is 8; load >= 0.6 needs more, SURVEY §0.3)")
+    ap.add_argument("--load", type=float, default=0.75, help="target table load factor")
+    ap.add_argument("--engine", choices=("auto", "table", "shards"), default="auto",
+                    help="one table, or hash-owner shards on this GPU (auto: shards once one "
+                         "table would outgrow the TLB reach)")
+    ap.add_argument("--shards", type=int, default=0, help="shard count (0 = auto)")
+    ap.add_argument("--no-status", action="store_true",
+                    help="exploration-only tables without the per-slot status array")
     ap.add_argument("--probe-group", type=int, default=0)
     ap.add_argument("--cache-slots", type=int, default=4096,
                     help="per-block shared-memory dedup cache entries (< 32 = off)")
@@ -339,14 +349,43 @@ def main():
     states_est = cf[0] if cf else None
     if states_est is None:
         raise SystemExit("workload without a closed form needs --states")
-    cap = table_capacity(states_est, vlen, args.bucket_words, args.load)
+    # engine: one table, or W hash-owner shards on this GPU when one table
+    # would outgrow the TLB reach (random access drops ~4x past ~64 GiB,
+    # profiles/README.md), each shard then stays inside it
+    est_bytes = table_capacity(states_est, vlen, args.bucket_words, args.load) * 4
+    shards = args.shards or (1 if args.engine == "table" or est_bytes <= TLB_REACH
+                             else -(-est_bytes // SHARD_BYTES))
+    per = states_est // shards + (states_est >> 8 if shards > 1 else 0)
+    cap = table_capacity(per, vlen, args.bucket_words, args.load)
     tcfg = TableConfig(bucket_words=args.bucket_words, num_hash_functions=args.hash_functions,
                        capacity_words=cap)
     cfg = ExploreConfig(table=tcfg, detect_deadlocks=True, probe_group=args.probe_group,
                         cache_slots=max(1, args.cache_slots), filter_log2=args.filter_log2)
     stream = torch.cuda.current_stream().cuda_stream
-    ex = Explorer(net, cfg, stream=stream)
-    table_bytes = ex.table.num_buckets * (4 * args.bucket_words + ((ex.table.slots_per_bucket + 7) & ~7))
+    from paper_1801_05857_b200.hashtable import slots_per_bucket
+    spb0 = slots_per_bucket(args.bucket_words, vlen, "half" if args.bucket_words == 32 else "plain")
+    status_bytes = cap // args.bucket_words * ((spb0 + 7) & ~7) * shards
+    aux_bytes = int(states_est * (0.035 + 0.12) * 4 * vlen) if shards > 1 else \
+        int(states_est * 0.035 * 4 * vlen)
+    # the per-slot status array (1 B per slot) only serves the claim / scan /
+    # dump API; drop it when the table plus its buffers would not fit with it
+    status = not args.no_status and \
+        cap * 4 * shards + status_bytes + aux_bytes < 0.97 * torch.cuda.mem_get_info()[0]
+    if shards == 1:
+        ex = Explorer(net, cfg, stream=stream, status=status)
+        total_slots = ex.table.total_slots
+        spb = ex.table.slots_per_bucket
+        nbk = ex.table.num_buckets
+    else:
+        from paper_1801_05857_b200.distributed import LocalShardExplorer
+        front = int(states_est * 0.035 / shards) + (1 << 20)
+        inbox = int(states_est * 0.12 / shards) + (1 << 20)
+        ex = LocalShardExplorer(net, cfg, shards, inbox_capacity=inbox, frontier_capacity=front,
+                                status=status, stream=stream)
+        total_slots = sum(sh.table.total_slots for sh in ex.shards)
+        spb = ex.shards[0].table.slots_per_bucket
+        nbk = sum(sh.table.num_buckets for sh in ex.shards)
+    table_bytes = nbk * (4 * args.bucket_words + (((spb + 7) & ~7) if status else 0))
 
     for _ in range(args.warmup):
         rep = ex.run()
@@ -369,7 +408,7 @@ def main():
     assert rep.outcome == "COMPLETE", rep.outcome
     value = rep.states * args.steps / (ms / 1e3)
 
-    # roofline of the dominant kernel (k_level), algorithmic bytes per step
+    # roofline of the level kernels, algorithmic bytes per step
     sbw = s_bw(args.bucket_words)
     alg_bytes = rep.transitions * sbw + rep.states * 12 * vlen
     level_ms = statistics.mean(r.level_ms for r in reps)
@@ -380,8 +419,17 @@ def main():
         traffic = tr.get(f"{args.workload}/bw{args.bucket_words}")
     ex.close()
 
-    # the random-access roofline R(g) on this GPU (32 GiB buffer >> L2)
+    # the random-access roofline R(g) on this GPU: a 32 GiB buffer (>> L2,
+    # inside the TLB reach) and, for tables beyond the reach, the table size
     ra = random_access()
+    table_gib = (table_bytes // shards) >> 30
+    ra_table = None
+    if table_gib > 48:
+        from paper_1801_05857_b200.bench import random_access_roofline
+        r128 = random_access_roofline(sbw, buffer_bytes=table_gib << 30)
+        ra_table = {"buffer_gib": table_gib, "g": sbw, "gbs": r128["gbs"],
+                    "accesses_per_s": r128["segments_per_sec"]}
+    r_peak = ra_table["gbs"] if ra_table else ra[sbw]["gbs"]
 
     # e2e through the public API with host buffers
     torch.cuda.synchronize()
@@ -389,13 +437,18 @@ def main():
     csr_bytes = None
     for i in range(args.e2e_steps + 1):
         t0 = time.perf_counter()
-        r = gx.explore(net, cfg)
+        if shards == 1:
+            r = gx.explore(net, cfg)
+        else:
+            from paper_1801_05857_b200.distributed import explore_local_shards
+            r = explore_local_shards(net, cfg, shards, inbox_capacity=inbox, frontier_capacity=front,
+                                     status=status)
         dt = time.perf_counter() - t0
         if i:
             e2e_times.append(dt)
     from paper_1801_05857_b200.explore import DeviceNetwork
     dn = DeviceNetwork(net, scheme)
-    csr_bytes = dn.csr_bytes + 4 * vlen
+    csr_bytes = (dn.csr_bytes + 4 * vlen) * shards
     dn.close()
     e2e_value = r.states * len(e2e_times) / sum(e2e_times) if e2e_times else None
 
@@ -416,27 +469,33 @@ def main():
             "vector_words": vlen, "bucket_words": args.bucket_words,
             "hash_functions": args.hash_functions, "table_bytes": table_bytes,
             "block_cache_slots": args.cache_slots, "l2_filter_log2": args.filter_log2,
-            "load_factor": rep.states / ex.table.total_slots,
+            "load_factor": rep.states / total_slots,
+            "status_array": status,
             "l2_policy": "table re-zeroed every step; table >> 126 MB L2",
-            "parallelism": "single GPU",
+            "parallelism": "single GPU" if shards == 1 else
+            f"single GPU, {shards} hash-owner shards (each table inside the TLB reach; "
+            "fused peer-routed levels)",
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
-                     "kernel": "k_level", "algorithmic_bytes_per_step": alg_bytes,
+                     "kernel": "k_level_staged" if shards == 1 else "k_level_routed + k_absorb",
+                     "algorithmic_bytes_per_step": alg_bytes,
                      "kernel_ms_per_step": level_ms,
                      "bytes_model": "transitions*max(32,4*bw) + states*12*vlen",
-                     "random_access_gbs": ra[sbw]["gbs"],
-                     "frac_of_random_access": achieved / ra[sbw]["gbs"],
-                     "random_access": ra},
+                     "random_access_gbs": r_peak,
+                     "frac_of_random_access": achieved / r_peak,
+                     "random_access": ra, "random_access_table_size": ra_table},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": csr_bytes,
                 "d2h_bytes_per_step": 64 + 400 * vlen,
-                "api": "paper_1801_05857_b200.explore(net, cfg) (allocates + frees the table)"},
+                "api": "paper_1801_05857_b200.explore(net, cfg) (allocates + frees the table)"
+                if shards == 1 else "distributed.explore_local_shards (allocates + frees the shards)"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "probes_per_step": rep.probes,
         "step_breakdown_ms": {"level_kernels": level_ms,
-                              "level_loop": statistics.mean(r.device_ms for r in reps),
+                              "level_loop": statistics.mean(r.device_ms for r in reps) if shards == 1
+                              else None,
                               "whole_step": ms / args.steps,
                               "max_frontier": rep.max_frontier},
     }

@@ -214,15 +214,24 @@ struct RouteArgs {
 
 // Send the keys of q[0, m) owned by other ranks to their inboxes; the
 // locally owned ones are compacted (stably) to the front of q.  Returns
-// their number; *routed counts keys sent (lane 0).
+// their number; *routed counts keys sent (lane 0).  scratch: 64 u32 of
+// per-warp shared memory (per-owner counts and cursors).  Lanes with the
+// same owner find each other with one match.any per 32 keys; each group's
+// lowest lane updates the owner's count / cursor (one writer per owner).
 template <int V>
 __device__ __forceinline__ uint32_t route_remote(const TableDesc& T, const RouteArgs& R, uint32_t* q,
                                                  uint32_t m, unsigned long long* ovf,
-                                                 unsigned long long* routed) {
+                                                 unsigned long long* routed, uint32_t* scratch) {
     const int lane = threadIdx.x & 31;
     const int world = R.world;
-    // pass 1: lane r counts the chunk's keys owned by rank r
-    uint32_t cnt = 0;
+    uint32_t* cnt = scratch;        // [GX_MAX_SHARDS]
+    uint32_t* cur = scratch + 32;   // [GX_MAX_SHARDS]
+    if (lane < GX_MAX_SHARDS) {
+        cnt[lane] = 0;
+        cur[lane] = 0;
+    }
+    __syncwarp();
+    // pass 1: keys per owner
     for (uint32_t r0 = 0; r0 < m; r0 += 32) {
         const uint32_t e = r0 + lane;
         int o = -1;
@@ -232,25 +241,24 @@ __device__ __forceinline__ uint32_t route_remote(const TableDesc& T, const Route
             for (int w = 0; w < V; w++) key[w] = q[e * V + w];
             o = owner_of(fold<V>(T.salt, key), world);
         }
-        for (int r = 0; r < world; r++) {
-            const uint32_t b = __ballot_sync(FULLMASK, o == r);
-            if (lane == r) cnt += __popc(b);
-        }
+        const uint32_t grp = __match_any_sync(FULLMASK, o);
+        if (o >= 0 && (grp & lanemask_lt()) == 0) cnt[o] += __popc(grp);
+        __syncwarp();
     }
     // reserve room in every peer inbox at once (independent remote atomics)
+    const uint32_t mine = lane < world ? cnt[lane] : 0u;
     unsigned long long base = 0;
     bool ok = true;
-    if (lane < world && lane != R.rank && cnt) {
-        base = atomicAdd(R.inbox_ctr[lane], (unsigned long long)cnt);
-        if (base + cnt > R.inbox_cap) {
+    if (lane < world && lane != R.rank && mine) {
+        base = atomicAdd(R.inbox_ctr[lane], (unsigned long long)mine);
+        if (base + mine > R.inbox_cap) {
             ok = false;
             atomicExch(ovf, 1ull);
         }
     }
-    const uint32_t sent = __reduce_add_sync(FULLMASK, lane != R.rank && lane < world ? cnt : 0u);
+    const uint32_t sent = __reduce_add_sync(FULLMASK, lane != R.rank ? mine : 0u);
     if (lane == 0) *routed += sent;
     // pass 2: scatter (peer stores, consecutive per owner) / compact local
-    uint32_t cur = 0, n_loc = 0;
     for (uint32_t r0 = 0; r0 < m; r0 += 32) {
         const uint32_t e = r0 + lane;
         int o = -1;
@@ -262,16 +270,13 @@ __device__ __forceinline__ uint32_t route_remote(const TableDesc& T, const Route
             for (int w = 0; w < V; w++) key[w] = q[e * V + w];
             o = owner_of(fold<V>(T.salt, key), world);
         }
-        uint32_t pos = 0;
-        for (int r = 0; r < world; r++) {
-            const uint32_t b = __ballot_sync(FULLMASK, o == r);
-            const uint32_t at = __shfl_sync(FULLMASK, cur, r);
-            if (o == r) pos = at + __popc(b & lanemask_lt());
-            if (lane == r) cur += __popc(b);
-        }
-        const unsigned long long b_o = __shfl_sync(FULLMASK, base, o < 0 ? 0 : o);
-        const int ok_o = __shfl_sync(FULLMASK, ok ? 1 : 0, o < 0 ? 0 : o);
+        const uint32_t grp = __match_any_sync(FULLMASK, o);
+        const uint32_t pos = (o >= 0 ? cur[o] : 0u) + __popc(grp & lanemask_lt());
+        const int src = o < 0 ? 0 : o;
+        const unsigned long long b_o = __shfl_sync(FULLMASK, base, src);
+        const int ok_o = __shfl_sync(FULLMASK, ok ? 1 : 0, src);
         __syncwarp();
+        if (o >= 0 && (grp & lanemask_lt()) == 0) cur[o] += __popc(grp);
         if (o >= 0 && o != R.rank) {
             if (ok_o) {
                 uint32_t* dst = R.inbox[o] + (b_o + pos) * (uint64_t)V;
@@ -285,8 +290,7 @@ __device__ __forceinline__ uint32_t route_remote(const TableDesc& T, const Route
         }
         __syncwarp();
     }
-    n_loc = __shfl_sync(FULLMASK, cur, R.rank);
-    return n_loc;
+    return cur[R.rank];
 }
 
 // The same level with the FINDORPUT of each successor chunk done by
@@ -369,7 +373,9 @@ __device__ __forceinline__ void level_staged_body(const TableDesc& T, const NetD
             uint32_t m = c1 - c0;
             if (cmask) m = cache_filter<V>(T, dcache, cmask, q, m);
             if (V <= 2 && A.gfilter_mask) m = global_filter<V>(T, A.gfilter, A.gfilter_mask, q, m);
-            if (ROUTE) m = route_remote<V>(T, R, q, m, &A.ctr[LV_OVF], &routed);
+            if (ROUTE)
+                m = route_remote<V>(T, R, q, m, &A.ctr[LV_OVF], &routed,
+                                    reinterpret_cast<uint32_t*>(stage));  // stage is idle here
             probes += lane == 0 ? m : 0;
             uint32_t full = 0;
             const uint32_t n_out = probe_staged<BW, V>(T, q, m, stage, sbkt, &full);

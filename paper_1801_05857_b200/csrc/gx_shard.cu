@@ -35,38 +35,44 @@ __global__ void __launch_bounds__(256, GX_STAGED_MINB) k_level_routed(TableDesc 
 }
 
 // FINDORPUT the inbox (n = *count keys, clamped to cap); inserted keys go to
-// the next frontier through the level's LevelArgs.
+// the next frontier through the level's LevelArgs.  Pure probing, nothing
+// to overlap it with: 128-thread blocks whose warps each keep ABSORB_KB
+// buckets in flight (4x the level kernel's batch).
+#ifndef GX_ABSORB_KB
+#define GX_ABSORB_KB 128
+#endif
 template <int BW, int V>
-__global__ void __launch_bounds__(256, GX_STAGED_MINB) k_absorb(TableDesc T, LevelArgs A, const uint32_t* __restrict__ inbox,
-                                                  const unsigned long long* count, uint64_t cap) {
-    using L = StagedSmem<BW, V>;
-    using S = Staged<BW, V>;
-    constexpr int QCAP = QWORDS / V;
+struct AbsorbSmem {
+    using S = Staged<BW, V, GX_ABSORB_KB>;
+    static constexpr size_t Q = 4ull * S::KB * V * 4;
+    static constexpr size_t B = 4ull * S::KB * 8;
+    static constexpr size_t ST = 4ull * S::STAGE_BYTES;
+    static constexpr size_t FIXED = Q + B + ST;
+};
+
+template <int BW, int V>
+__global__ void __launch_bounds__(128) k_absorb(TableDesc T, LevelArgs A, const uint32_t* __restrict__ inbox,
+                                                const unsigned long long* count, uint64_t cap) {
+    using L = AbsorbSmem<BW, V>;
+    using S = Staged<BW, V, GX_ABSORB_KB>;
+    constexpr int KB = S::KB;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * QWORDS;
-    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::KB;
+    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * (KB * V);
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * KB;
     uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
-    unsigned long long* dcache = reinterpret_cast<unsigned long long*>(smem + L::FIXED);
-    const uint32_t cmask = V <= 2 ? A.cache_mask : 0u;
-    if (cmask) {
-        for (uint32_t i = threadIdx.x; i <= cmask; i += blockDim.x) dcache[i] = 0ull;
-        __syncthreads();
-    }
     const uint64_t n = min((uint64_t)*count, cap);
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
     unsigned long long probes = 0;
-    for (uint64_t base = warp * QCAP; base < n; base += nwarps * QCAP) {
-        const uint32_t m0 = (uint32_t)min((uint64_t)QCAP, n - base);
-        for (uint32_t x = lane; x < m0 * V; x += 32) q[x] = __ldcs(inbox + base * V + x);
+    for (uint64_t base = warp * KB; base < n; base += nwarps * KB) {
+        const uint32_t m = (uint32_t)min((uint64_t)KB, n - base);
+        for (uint32_t x = lane; x < m * V; x += 32) q[x] = __ldcs(inbox + base * V + x);
         __syncwarp();
-        uint32_t m = m0;
-        if (cmask) m = cache_filter<V>(T, dcache, cmask, q, m);
         probes += lane == 0 ? m : 0;
         uint32_t full = 0;
-        const uint32_t n_out = probe_staged<BW, V>(T, q, m, stage, sbkt, &full);
+        const uint32_t n_out = probe_staged<BW, V, GX_ABSORB_KB>(T, q, m, stage, sbkt, &full);
         if (__any_sync(FULLMASK, full != 0u) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
         if (n_out) flush_out<V>(A, q, n_out);
         __syncwarp();
@@ -81,17 +87,18 @@ typedef void (*absorb_kernel_t)(TableDesc, LevelArgs, const uint32_t*, const uns
 struct ShardKernels {
     routed_kernel_t a;
     absorb_kernel_t b;
-    size_t fixed_smem;
+    size_t fixed_smem;   // kernel A's dynamic shared memory besides the cache
+    size_t absorb_smem;  // kernel B's
 };
 
 template <int BW>
 static ShardKernels pick_shard_v(int v) {
     switch (v) {
-        case 1: return {k_level_routed<BW, 1>, k_absorb<BW, 1>, StagedSmem<BW, 1>::FIXED};
-        case 2: return {k_level_routed<BW, 2>, k_absorb<BW, 2>, StagedSmem<BW, 2>::FIXED};
-        case 4: return {k_level_routed<BW, 4>, k_absorb<BW, 4>, StagedSmem<BW, 4>::FIXED};
+        case 1: return {k_level_routed<BW, 1>, k_absorb<BW, 1>, StagedSmem<BW, 1>::FIXED, AbsorbSmem<BW, 1>::FIXED};
+        case 2: return {k_level_routed<BW, 2>, k_absorb<BW, 2>, StagedSmem<BW, 2>::FIXED, AbsorbSmem<BW, 2>::FIXED};
+        case 4: return {k_level_routed<BW, 4>, k_absorb<BW, 4>, StagedSmem<BW, 4>::FIXED, AbsorbSmem<BW, 4>::FIXED};
     }
-    return {nullptr, nullptr, 0};
+    return {nullptr, nullptr, 0, 0};
 }
 
 static ShardKernels pick_shard(const TableDesc& T) {
@@ -101,7 +108,7 @@ static ShardKernels pick_shard(const TableDesc& T) {
         case 16: return pick_shard_v<16>((int)T.vlen);
         case 32: return pick_shard_v<32>((int)T.vlen);
     }
-    return {nullptr, nullptr, 0};
+    return {nullptr, nullptr, 0, 0};
 }
 
 static constexpr size_t INBOX_HEAD = 256;  // counter cell, padded
@@ -138,7 +145,7 @@ struct gx_shard {
     uint64_t n_pending = 0;
     LevelArgs A;
     std::vector<uint32_t> kept, dlhost;
-    cudaEvent_t e0, e1, e2;
+    cudaEvent_t e0, e1, e2, e3;  // kernel A: e0..e1, kernel B: e2..e3
     double level_ms = 0;
     int32_t detect = 0;
 };
@@ -209,10 +216,12 @@ int gx_shard_create(gx_net* n, gx_table* t, int32_t rank, int32_t world, uint64_
     }
     GX_CUDA(cudaMemsetAsync(s->inbox_block, 0, INBOX_HEAD, s->stream));
     GX_CUDA(cudaFuncSetAttribute((const void*)K.a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem));
-    GX_CUDA(cudaFuncSetAttribute((const void*)K.b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem));
+    GX_CUDA(cudaFuncSetAttribute((const void*)K.b, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)K.absorb_smem));
     GX_CUDA(cudaEventCreate(&s->e0));
     GX_CUDA(cudaEventCreate(&s->e1));
     GX_CUDA(cudaEventCreate(&s->e2));
+    GX_CUDA(cudaEventCreate(&s->e3));
     *out = s;
     return GX_OK;
 }
@@ -228,6 +237,7 @@ int gx_shard_destroy(gx_shard* s) {
     cudaEventDestroy(s->e0);
     cudaEventDestroy(s->e1);
     cudaEventDestroy(s->e2);
+    cudaEventDestroy(s->e3);
     delete s;
     return GX_OK;
 }
@@ -361,19 +371,25 @@ int gx_shard_absorb(gx_shard* s, uint64_t* stats) {
     cudaStream_t st = s->stream;
     // the inbox fill is only known on the device: a persistent grid that
     // exits at once when nothing arrived
-    s->K.b<<<sm_count() * GX_STAGED_MINB, 256, s->smem, st>>>(t->d, s->A, s->R.inbox[s->rank],
-                                                 s->R.inbox_ctr[s->rank], s->inbox_cap);
-    GX_LAUNCHED();
     GX_CUDA(cudaEventRecord(s->e2, st));
+    int bpm = 0;  // resident absorb blocks per SM
+    GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, s->K.b, 128, s->K.absorb_smem));
+    s->K.b<<<sm_count() * std::max(bpm, 1), 128, s->K.absorb_smem, st>>>(t->d, s->A, s->R.inbox[s->rank],
+                                                                        s->R.inbox_ctr[s->rank], s->inbox_cap);
+    GX_LAUNCHED();
+    GX_CUDA(cudaEventRecord(s->e3, st));
     unsigned long long* hc = (unsigned long long*)t->h_ctr;
     unsigned long long inbox_n = 0;
     GX_CUDA(cudaMemcpyAsync(hc, t->d_ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaMemcpyAsync(&inbox_n, s->R.inbox_ctr[s->rank], 8, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaMemsetAsync(s->R.inbox_ctr[s->rank], 0, 8, st));
     GX_CUDA(cudaStreamSynchronize(st));
-    float ms = 0;
-    GX_CUDA(cudaEventElapsedTime(&ms, s->e0, s->e2));
-    s->level_ms += ms;
+    // device time of this shard's two kernels (other shards' kernels may run
+    // between them on a shared stream)
+    float ma = 0, mb = 0;
+    GX_CUDA(cudaEventElapsedTime(&ma, s->e0, s->e1));
+    GX_CUDA(cudaEventElapsedTime(&mb, s->e2, s->e3));
+    s->level_ms += ma + mb;
     const uint64_t claims = s->nF;
     const uint64_t nnew = hc[LV_NEW] - s->new_base;
     s->new_base = hc[LV_NEW];

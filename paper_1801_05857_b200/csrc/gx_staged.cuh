@@ -110,13 +110,16 @@ __device__ __forceinline__ int probe_lane(const TableDesc& T, const uint32_t* km
     return TABLE_FULL;
 }
 
-template <int BW, int V>
+// KBX > 0 overrides the batch size (the absorb kernel, which has no
+// expansion to overlap, keeps more buckets in flight per warp)
+template <int BW, int V, int KBX = 0>
 struct Staged {
     static constexpr int CH = BW / 4;                 // 16-byte chunks per bucket
     static constexpr int SPB = BW / V;                // slots per bucket
     static constexpr int SPC = 4 / V;                 // slots per chunk
-    static constexpr int KB = GX_STAGE_BYTES / (4 * BW) > GX_STAGE_KB_MAX ? GX_STAGE_KB_MAX
-                                                                          : GX_STAGE_BYTES / (4 * BW);
+    static constexpr int KB = KBX > 0 ? KBX
+                              : (GX_STAGE_BYTES / (4 * BW) > GX_STAGE_KB_MAX ? GX_STAGE_KB_MAX
+                                                                             : GX_STAGE_BYTES / (4 * BW));
     static constexpr int STAGE_BYTES = KB * 4 * BW;   // per warp
     static constexpr int KPL = KB / 32;               // keys per lane per batch
 };
@@ -126,11 +129,11 @@ struct Staged {
 // only ever written at or below the position it was read from); returns
 // their number.  *full counts (per lane) the keys that hit TABLE_FULL.  stage: this
 // warp's STAGE_BYTES of shared memory; sbkt: its KB bucket indices.
-template <int BW, int V>
+template <int BW, int V, int KBX = 0>
 __device__ __forceinline__ uint32_t probe_staged(const TableDesc& T, uint32_t* q, uint32_t m,
                                                  uint4* stage, unsigned long long* sbkt,
                                                  uint32_t* full) {
-    using S = Staged<BW, V>;
+    using S = Staged<BW, V, KBX>;
     constexpr int KB = S::KB, KPL = S::KPL, CH = S::CH, SPC = S::SPC;
     constexpr unsigned long long SKIP = ~0ull;
     const int lane = threadIdx.x & 31;

@@ -253,7 +253,7 @@ def connect_local(shards):
     check(lib().gx_shard_connect_local(arr, len(shards)))
 
 
-def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None) -> ShardResult:
+def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None):
     """The level protocol shared by the in-process and multi-process
     drivers: every shard expands, a barrier, every shard absorbs, the
     level's stats are reduced over all ranks (explore.py:251-265)."""
@@ -285,12 +285,58 @@ def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None) -> S
                 break
     tot = np.zeros(5, np.uint64)
     kept = []
+    level_ms = 0.0
     for s in shards:
         rep, k = s.finish()
         tot += np.array([rep.states, rep.transitions, rep.expanded, rep.deadlocks_total, rep.probes],
                         np.uint64)
+        level_ms += rep.level_ms
         kept.extend(k)
-    return tot, sorted(kept)[:100], rounds, outcome
+    return tot, sorted(kept)[:100], rounds, outcome, level_ms
+
+
+class LocalShardExplorer:
+    """`world` hash-owner shards of one network in this process (one GPU),
+    built once and explored any number of times (each run clears the
+    tables).  On one GPU this keeps every shard's random probes inside the
+    TLB reach (profiles/README.md: random access drops from 36 to 9 G/s
+    once a table outgrows ~64 GiB); across GPUs it is the same protocol
+    with peer inboxes over NVLink."""
+
+    def __init__(self, net, cfg, world: int, inbox_capacity: int = 0, frontier_capacity: int = 0,
+                 status: bool = True, stream=None):
+        self.cfg = cfg
+        self.shards = []
+        try:
+            for r in range(world):
+                self.shards.append(FusedShard(net, cfg, r, world, inbox_capacity, frontier_capacity,
+                                              stream=stream, status=status))
+            connect_local(self.shards)
+        except Exception:
+            self.close()
+            raise
+
+    def run(self):
+        import time
+
+        from .explore import ExplorationReport
+
+        t0 = time.perf_counter()
+        tot, kept, rounds, outcome, level_ms = _run_levels(self.shards, lambda: None, lambda a: a,
+                                                           self.cfg.detect_deadlocks,
+                                                           self.cfg.max_iterations)
+        wall = time.perf_counter() - t0
+        states = int(tot[0])
+        return ExplorationReport(
+            states=states, transitions=int(tot[1]), deadlocks=tuple(kept),
+            deadlocks_total=int(tot[3]), expanded=int(tot[2]), iterations=rounds, wall_time=wall,
+            throughput=states / wall if wall > 0 else 0.0, outcome=outcome, probes=int(tot[4]),
+            level_ms=float(level_ms))
+
+    def close(self):
+        for s in self.shards:
+            s.close()
+        self.shards = []
 
 
 def explore_local_shards(net, cfg, world: int, inbox_capacity: int = 0, frontier_capacity: int = 0,
@@ -299,26 +345,11 @@ def explore_local_shards(net, cfg, world: int, inbox_capacity: int = 0, frontier
     process (one GPU): the multi-GPU protocol and kernels, with peer
     inboxes as local device memory.  Returns an ExplorationReport; its
     results equal explore(net, cfg)'s."""
-    import time
-
-    from .explore import ExplorationReport
-
-    shards = [FusedShard(net, cfg, r, world, inbox_capacity, frontier_capacity, status=status)
-              for r in range(world)]
+    ex = LocalShardExplorer(net, cfg, world, inbox_capacity, frontier_capacity, status=status)
     try:
-        connect_local(shards)
-        t0 = time.perf_counter()
-        tot, kept, rounds, outcome = _run_levels(shards, lambda: None, lambda a: a,
-                                                 cfg.detect_deadlocks, cfg.max_iterations)
-        wall = time.perf_counter() - t0
-        states = int(tot[0])
-        return ExplorationReport(
-            states=states, transitions=int(tot[1]), deadlocks=tuple(kept),
-            deadlocks_total=int(tot[3]), expanded=int(tot[2]), iterations=rounds, wall_time=wall,
-            throughput=states / wall if wall > 0 else 0.0, outcome=outcome, probes=int(tot[4]))
+        return ex.run()
     finally:
-        for s in shards:
-            s.close()
+        ex.close()
 
 
 def explore_fused(shard: FusedShard, dist, torch, detect: bool, max_iterations=None,
@@ -337,7 +368,7 @@ def explore_fused(shard: FusedShard, dist, torch, detect: bool, max_iterations=N
         dist.all_reduce(t)
         return t.cpu().numpy().astype(np.uint64)
 
-    tot, kept, rounds, outcome = _run_levels([shard], barrier, reduce, detect, max_iterations)
+    tot, kept, rounds, outcome, _ = _run_levels([shard], barrier, reduce, detect, max_iterations)
     tot = reduce(tot)
     gathered = [None] * dist.get_world_size()
     dist.all_gather_object(gathered, kept)

@@ -239,7 +239,7 @@ class OracleFusedShard:
             pass
         r = Rep()
         r.states, r.transitions, r.expanded = self.states, self.trans, self.expanded
-        r.deadlocks_total, r.probes = self.dl_total, 0
+        r.deadlocks_total, r.probes, r.level_ms = self.dl_total, 0, 0.0
         return r, sorted(self.kept)[:100]
 
 

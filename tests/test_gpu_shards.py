@@ -73,3 +73,31 @@ def test_sharded_generated_models(tmp_path):
         rep = D.explore_local_shards(gx.load_network(p), _cfg(cap=1 << 24), 3)
         assert (rep.states, rep.transitions, rep.iterations - 1, rep.deadlocks_total) == \
             (want["states"], want["transitions"], want["levels"], want["deadlocks"])
+
+
+@pytest.mark.parametrize("bw", [4, 8, 32])
+@pytest.mark.parametrize("world", [3, 4])
+def test_sharded_contention(bw, world, tmp_path):
+    """Token ring N=13 split over shards whose tables run at load ~0.7 with
+    K=32: lost CASes, staged rehash rounds and inbox routing together; the
+    exploration-only (no status array) tables are used as in the 150 GB
+    bench configuration."""
+    from paper_1801_05857_b200.bench import gen_token_ring
+    from paper_1801_05857_b200.hashtable import slots_per_bucket
+    n = 13
+    _, p = gen_token_ring(n, tmp_path / "ring")
+    net = gx.load_network(p)
+    states = 2 * n * 3 ** (n - 1)
+    spb = slots_per_bucket(bw, 2, "half" if bw == 32 else "plain")
+    cap = (int(states / world / 0.7 / spb) + 256) * bw
+    cfg = ExploreConfig(table=TableConfig(bucket_words=bw, num_hash_functions=32, capacity_words=cap),
+                        detect_deadlocks=True)
+    ex = D.LocalShardExplorer(net, cfg, world, inbox_capacity=states // 2, frontier_capacity=states // 4,
+                              status=False)
+    try:
+        for _ in range(2):
+            rep = ex.run()
+            assert (rep.states, rep.transitions, rep.iterations, rep.outcome) == \
+                (states, 4 * n * n * 3 ** (n - 2), 6 * n - 4 + 1, "COMPLETE")
+    finally:
+        ex.close()
