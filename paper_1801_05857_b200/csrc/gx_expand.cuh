@@ -89,7 +89,7 @@ __device__ __forceinline__ uint32_t expand_state(const NetDesc& N, const uint32_
     uint32_t n = 0;
     uint32_t t[V];
     for (uint32_t i = 0; i < N.nproc; i++) {
-        const uint4 pr = __ldg(&N.proc[i]);
+        const uint4 pr = i < GX_PROC_INLINE ? N.proc_c[i] : __ldg(&N.proc[i]);
         const uint32_t q = field_get<V>(s, pr.x, pr.y, pr.z);
         const uint4 e = __ldg(&N.qtab[pr.w + q]);
         count += e.z;
@@ -105,9 +105,13 @@ __device__ __forceinline__ uint32_t expand_state(const NetDesc& N, const uint32_
             }
         }
         n += e.y;
-        const uint32_t nt = __ldg(&N.trig[e.w]);
+        // packed: the trigger count rides in qtab, so states that trigger no
+        // rule (most of them) skip the dependent load of the trigger list
+        const uint32_t toff = N.trig_packed ? (e.w & 0xffffffu) : e.w;
+        uint32_t nt = N.trig_packed ? (e.w >> 24) : 255u;
+        if (nt == 255u) nt = __ldg(&N.trig[toff]);
         for (uint32_t x = 0; x < nt; x++) {
-            const uint32_t r = __ldg(&N.trig[e.w + 1 + x]);
+            const uint32_t r = __ldg(&N.trig[toff + 1 + x]);
             const uint4 rl = __ldg(&N.rules[r]);
             uint64_t combos = 1;
             for (uint32_t k = 0; k < rl.x; k++) {

@@ -792,6 +792,17 @@ int gx_net_create(const gx_network_csr* c, void* stream, gx_net** out) {
     std::vector<uint32_t> blob(off[9] + 4, 0u);
     for (int i = 0; i < 9; i++)
         if (len[i]) memcpy(blob.data() + off[i], src[i], sizeof(uint32_t) * len[i]);
+    // pack each qtab entry's trigger count next to its offset when all
+    // offsets fit in 24 bits (255 = read the count from the list)
+    bool packed = c->n_trig < (1ull << 24);
+    if (packed) {
+        uint32_t* q = blob.data() + off[1];
+        for (uint64_t e = 0; e + 3 < c->n_qtab; e += 4) {
+            const uint32_t toff = q[e + 3];
+            const uint32_t nt = c->trig[toff];
+            q[e + 3] = toff | (std::min<uint32_t>(nt, 255u) << 24);
+        }
+    }
     cudaError_t e = cudaMalloc(&n->d_blob, sizeof(uint32_t) * blob.size());
     if (e == cudaSuccess) e = cudaMalloc(&n->d_initial, sizeof(uint32_t) * 16);
     if (e != cudaSuccess) {
@@ -817,6 +828,10 @@ int gx_net_create(const gx_network_csr* c, void* stream, gx_net** out) {
     d.nproc = c->nproc;
     d.nrules = c->nrules;
     d.vlen = c->vlen;
+    d.trig_packed = packed ? 1u : 0u;
+    memset(d.proc_c, 0, sizeof d.proc_c);
+    for (uint32_t i = 0; i < c->nproc && i < GX_PROC_INLINE; i++)
+        d.proc_c[i] = make_uint4(c->proc[4 * i], c->proc[4 * i + 1], c->proc[4 * i + 2], c->proc[4 * i + 3]);
     *out = n;
     return GX_OK;
 }

@@ -34,9 +34,12 @@ int sm_count();
     } while (0)
 
 // Device network, network.py:43-62 flattened (see gx.h gx_network_csr).
+#define GX_PROC_INLINE 32  // processes whose descriptors ride in the kernel parameters
+
 struct NetDesc {
     const uint4* proc;   // {word, shift, mask, qbase}
-    const uint4* qtab;   // per (proc, state): {im_off, im_n, im_cnt, trig_off}
+    const uint4* qtab;   // per (proc, state): {im_off, im_n, im_cnt, trig}; trig =
+                         // trig_off | nt << 24 when trig_packed (nt < 255), else trig_off
     const uint32_t* im_dst;
     const uint32_t* trig;   // [n, rule...]
     const uint4* rules;     // {npart, part_off, dedup_off, result}
@@ -44,7 +47,11 @@ struct NetDesc {
     const uint2* rq;        // {off, n}
     const uint32_t* rdst;
     const uint32_t* dedup;  // [n, rule...]
-    uint32_t nproc, nrules, vlen, pad;
+    uint32_t nproc, nrules, vlen, trig_packed;
+    // the first GX_PROC_INLINE process descriptors again, in the parameter
+    // (constant) bank: the expansion loop walks them in lockstep across the
+    // warp, so a uniform constant load replaces an L1 round trip
+    uint4 proc_c[GX_PROC_INLINE];
 };
 
 // A growable device scratch buffer.
