@@ -65,6 +65,10 @@ def parse():
                     help="one table, or hash-owner shards on this GPU (auto: shards once one "
                          "table would outgrow the TLB reach)")
     ap.add_argument("--shards", type=int, default=0, help="shard count (0 = auto)")
+    ap.add_argument("--inbox-frac", type=float, default=0.12,
+                    help="sharded engine: inbox keys per shard = frac * states / shards")
+    ap.add_argument("--frontier-frac", type=float, default=0.035,
+                    help="frontier vectors per shard = frac * states / shards")
     ap.add_argument("--no-status", action="store_true",
                     help="exploration-only tables without the per-slot status array")
     ap.add_argument("--probe-group", type=int, default=0)
@@ -365,8 +369,8 @@ def main():
     from paper_1801_05857_b200.hashtable import slots_per_bucket
     spb0 = slots_per_bucket(args.bucket_words, vlen, "half" if args.bucket_words == 32 else "plain")
     status_bytes = cap // args.bucket_words * ((spb0 + 7) & ~7) * shards
-    aux_bytes = int(states_est * (0.035 + 0.12) * 4 * vlen) if shards > 1 else \
-        int(states_est * 0.035 * 4 * vlen)
+    aux_bytes = int(states_est * (args.frontier_frac + args.inbox_frac) * 4 * vlen) if shards > 1 else \
+        int(states_est * args.frontier_frac * 4 * vlen)
     # the per-slot status array (1 B per slot) only serves the claim / scan /
     # dump API; drop it when the table plus its buffers would not fit with it
     status = not args.no_status and \
@@ -378,8 +382,8 @@ def main():
         nbk = ex.table.num_buckets
     else:
         from paper_1801_05857_b200.distributed import LocalShardExplorer
-        front = int(states_est * 0.035 / shards) + (1 << 20)
-        inbox = int(states_est * 0.12 / shards) + (1 << 20)
+        front = int(states_est * args.frontier_frac / shards) + (1 << 20)
+        inbox = int(states_est * args.inbox_frac / shards) + (1 << 20)
         ex = LocalShardExplorer(net, cfg, shards, inbox_capacity=inbox, frontier_capacity=front,
                                 status=status, stream=stream)
         total_slots = sum(sh.table.total_slots for sh in ex.shards)

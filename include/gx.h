@@ -265,6 +265,15 @@ int gx_shard_connect_local(gx_shard *const *shards, int32_t world);
 int gx_shard_begin(gx_shard *s, int32_t owns_initial, int32_t detect_deadlocks, int32_t *table_full);
 int gx_shard_expand(gx_shard *s);
 int gx_shard_absorb(gx_shard *s, uint64_t *stats);
+/* The same level in frontier chunks, so inboxes stay bounded: for each
+ * chunk every shard calls gx_shard_expand_range (states [begin, begin +
+ * count) of its current frontier), a barrier, then gx_shard_absorb_chunk;
+ * after the last chunk gx_shard_end_level returns the level's stats.
+ * gx_shard_frontier gives the current frontier size. */
+int gx_shard_expand_range(gx_shard *s, uint64_t begin, uint64_t count);
+int gx_shard_absorb_chunk(gx_shard *s);
+int gx_shard_end_level(gx_shard *s, uint64_t *stats);
+int gx_shard_frontier(const gx_shard *s, uint64_t *n);
 /* finalise statuses; local report (states, transitions, expanded,
  * deadlocks of this shard; level_ms = its device time) */
 int gx_shard_finish(gx_shard *s, gx_report *report, uint32_t *deadlocks);

@@ -101,6 +101,10 @@ SIGNATURES = {
     "gx_shard_begin": (C.c_int, [_vp, C.c_int32, C.c_int32, _i32p]),
     "gx_shard_expand": (C.c_int, [_vp]),
     "gx_shard_absorb": (C.c_int, [_vp, _u64p]),
+    "gx_shard_expand_range": (C.c_int, [_vp, C.c_uint64, C.c_uint64]),
+    "gx_shard_absorb_chunk": (C.c_int, [_vp]),
+    "gx_shard_end_level": (C.c_int, [_vp, _u64p]),
+    "gx_shard_frontier": (C.c_int, [_vp, _u64p]),
     "gx_shard_finish": (C.c_int, [_vp, _P(Report), _u32p]),
     "gx_random_access_bench_alloc": (C.c_int, [C.c_uint64, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
                                                C.c_int32, _P(C.c_double), _P(C.c_double), _u64p]),

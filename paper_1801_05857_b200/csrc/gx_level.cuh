@@ -224,6 +224,13 @@ __device__ __forceinline__ uint32_t route_remote(const TableDesc& T, const Route
                                                  unsigned long long* routed, uint32_t* scratch) {
     const int lane = threadIdx.x & 31;
     const int world = R.world;
+    // GX_ROUTE_ALL: own keys go through the own inbox too, so every probe
+    // happens in the absorb kernel (a B200 experiment; off by default)
+#ifdef GX_ROUTE_ALL
+    const int self = -1;
+#else
+    const int self = R.rank;
+#endif
     uint32_t* cnt = scratch;        // [GX_MAX_SHARDS]
     uint32_t* cur = scratch + 32;   // [GX_MAX_SHARDS]
     if (lane < GX_MAX_SHARDS) {
@@ -249,14 +256,14 @@ __device__ __forceinline__ uint32_t route_remote(const TableDesc& T, const Route
     const uint32_t mine = lane < world ? cnt[lane] : 0u;
     unsigned long long base = 0;
     bool ok = true;
-    if (lane < world && lane != R.rank && mine) {
+    if (lane < world && lane != self && mine) {
         base = atomicAdd(R.inbox_ctr[lane], (unsigned long long)mine);
         if (base + mine > R.inbox_cap) {
             ok = false;
             atomicExch(ovf, 1ull);
         }
     }
-    const uint32_t sent = __reduce_add_sync(FULLMASK, lane != R.rank ? mine : 0u);
+    const uint32_t sent = __reduce_add_sync(FULLMASK, lane != self ? mine : 0u);
     if (lane == 0) *routed += sent;
     // pass 2: scatter (peer stores, consecutive per owner) / compact local
     for (uint32_t r0 = 0; r0 < m; r0 += 32) {
@@ -277,20 +284,20 @@ __device__ __forceinline__ uint32_t route_remote(const TableDesc& T, const Route
         const int ok_o = __shfl_sync(FULLMASK, ok ? 1 : 0, src);
         __syncwarp();
         if (o >= 0 && (grp & lanemask_lt()) == 0) cur[o] += __popc(grp);
-        if (o >= 0 && o != R.rank) {
+        if (o >= 0 && o != self) {
             if (ok_o) {
                 uint32_t* dst = R.inbox[o] + (b_o + pos) * (uint64_t)V;
 #pragma unroll
                 for (int w = 0; w < V; w++) dst[w] = key[w];
             }
-        } else if (o == R.rank) {
+        } else if (o == self) {
             // pos counts this rank's keys so far: a stable in-place compaction
 #pragma unroll
             for (int w = 0; w < V; w++) q[pos * V + w] = key[w];
         }
         __syncwarp();
     }
-    return cur[R.rank];
+    return self < 0 ? 0u : cur[self];
 }
 
 // The same level with the FINDORPUT of each successor chunk done by

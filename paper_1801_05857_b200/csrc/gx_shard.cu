@@ -35,44 +35,38 @@ __global__ void __launch_bounds__(256, GX_STAGED_MINB) k_level_routed(TableDesc 
 }
 
 // FINDORPUT the inbox (n = *count keys, clamped to cap); inserted keys go to
-// the next frontier through the level's LevelArgs.  Pure probing, nothing
-// to overlap it with: 128-thread blocks whose warps each keep ABSORB_KB
-// buckets in flight (4x the level kernel's batch).
-#ifndef GX_ABSORB_KB
-#define GX_ABSORB_KB 128
-#endif
+// the next frontier through the level's LevelArgs.
 template <int BW, int V>
-struct AbsorbSmem {
-    using S = Staged<BW, V, GX_ABSORB_KB>;
-    static constexpr size_t Q = 4ull * S::KB * V * 4;
-    static constexpr size_t B = 4ull * S::KB * 8;
-    static constexpr size_t ST = 4ull * S::STAGE_BYTES;
-    static constexpr size_t FIXED = Q + B + ST;
-};
-
-template <int BW, int V>
-__global__ void __launch_bounds__(128) k_absorb(TableDesc T, LevelArgs A, const uint32_t* __restrict__ inbox,
-                                                const unsigned long long* count, uint64_t cap) {
-    using L = AbsorbSmem<BW, V>;
-    using S = Staged<BW, V, GX_ABSORB_KB>;
-    constexpr int KB = S::KB;
+__global__ void __launch_bounds__(256, GX_STAGED_MINB) k_absorb(TableDesc T, LevelArgs A, const uint32_t* __restrict__ inbox,
+                                                  const unsigned long long* count, uint64_t cap) {
+    using L = StagedSmem<BW, V>;
+    using S = Staged<BW, V>;
+    constexpr int QCAP = QWORDS / V;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * (KB * V);
-    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * KB;
+    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * QWORDS;
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::KB;
     uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
+    unsigned long long* dcache = reinterpret_cast<unsigned long long*>(smem + L::FIXED);
+    const uint32_t cmask = V <= 2 ? A.cache_mask : 0u;
+    if (cmask) {
+        for (uint32_t i = threadIdx.x; i <= cmask; i += blockDim.x) dcache[i] = 0ull;
+        __syncthreads();
+    }
     const uint64_t n = min((uint64_t)*count, cap);
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
     unsigned long long probes = 0;
-    for (uint64_t base = warp * KB; base < n; base += nwarps * KB) {
-        const uint32_t m = (uint32_t)min((uint64_t)KB, n - base);
-        for (uint32_t x = lane; x < m * V; x += 32) q[x] = __ldcs(inbox + base * V + x);
+    for (uint64_t base = warp * QCAP; base < n; base += nwarps * QCAP) {
+        const uint32_t m0 = (uint32_t)min((uint64_t)QCAP, n - base);
+        for (uint32_t x = lane; x < m0 * V; x += 32) q[x] = __ldcs(inbox + base * V + x);
         __syncwarp();
+        uint32_t m = m0;
+        if (cmask) m = cache_filter<V>(T, dcache, cmask, q, m);
         probes += lane == 0 ? m : 0;
         uint32_t full = 0;
-        const uint32_t n_out = probe_staged<BW, V, GX_ABSORB_KB>(T, q, m, stage, sbkt, &full);
+        const uint32_t n_out = probe_staged<BW, V>(T, q, m, stage, sbkt, &full);
         if (__any_sync(FULLMASK, full != 0u) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
         if (n_out) flush_out<V>(A, q, n_out);
         __syncwarp();
@@ -87,18 +81,17 @@ typedef void (*absorb_kernel_t)(TableDesc, LevelArgs, const uint32_t*, const uns
 struct ShardKernels {
     routed_kernel_t a;
     absorb_kernel_t b;
-    size_t fixed_smem;   // kernel A's dynamic shared memory besides the cache
-    size_t absorb_smem;  // kernel B's
+    size_t fixed_smem;  // dynamic shared memory besides the cache (both kernels)
 };
 
 template <int BW>
 static ShardKernels pick_shard_v(int v) {
     switch (v) {
-        case 1: return {k_level_routed<BW, 1>, k_absorb<BW, 1>, StagedSmem<BW, 1>::FIXED, AbsorbSmem<BW, 1>::FIXED};
-        case 2: return {k_level_routed<BW, 2>, k_absorb<BW, 2>, StagedSmem<BW, 2>::FIXED, AbsorbSmem<BW, 2>::FIXED};
-        case 4: return {k_level_routed<BW, 4>, k_absorb<BW, 4>, StagedSmem<BW, 4>::FIXED, AbsorbSmem<BW, 4>::FIXED};
+        case 1: return {k_level_routed<BW, 1>, k_absorb<BW, 1>, StagedSmem<BW, 1>::FIXED};
+        case 2: return {k_level_routed<BW, 2>, k_absorb<BW, 2>, StagedSmem<BW, 2>::FIXED};
+        case 4: return {k_level_routed<BW, 4>, k_absorb<BW, 4>, StagedSmem<BW, 4>::FIXED};
     }
-    return {nullptr, nullptr, 0, 0};
+    return {nullptr, nullptr, 0};
 }
 
 static ShardKernels pick_shard(const TableDesc& T) {
@@ -108,7 +101,7 @@ static ShardKernels pick_shard(const TableDesc& T) {
         case 16: return pick_shard_v<16>((int)T.vlen);
         case 32: return pick_shard_v<32>((int)T.vlen);
     }
-    return {nullptr, nullptr, 0, 0};
+    return {nullptr, nullptr, 0};
 }
 
 static constexpr size_t INBOX_HEAD = 256;  // counter cell, padded
@@ -148,6 +141,8 @@ struct gx_shard {
     cudaEvent_t e0, e1, e2, e3;  // kernel A: e0..e1, kernel B: e2..e3
     double level_ms = 0;
     int32_t detect = 0;
+    bool level_open = false;      // LevelArgs of the current level are set
+    bool inbox_overflow = false;  // some chunk overflowed the inbox
 };
 
 extern "C" {
@@ -216,8 +211,7 @@ int gx_shard_create(gx_net* n, gx_table* t, int32_t rank, int32_t world, uint64_
     }
     GX_CUDA(cudaMemsetAsync(s->inbox_block, 0, INBOX_HEAD, s->stream));
     GX_CUDA(cudaFuncSetAttribute((const void*)K.a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem));
-    GX_CUDA(cudaFuncSetAttribute((const void*)K.b, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)K.absorb_smem));
+    GX_CUDA(cudaFuncSetAttribute((const void*)K.b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem));
     GX_CUDA(cudaEventCreate(&s->e0));
     GX_CUDA(cudaEventCreate(&s->e1));
     GX_CUDA(cudaEventCreate(&s->e2));
@@ -310,6 +304,8 @@ int gx_shard_begin(gx_shard* s, int32_t owns_initial, int32_t detect_deadlocks, 
     s->kept.clear();
     s->level_ms = 0;
     s->detect = detect_deadlocks;
+    s->level_open = false;
+    s->inbox_overflow = false;
     *table_full = 0;
     if (owns_initial) {
         rc = t->codes.ensure(16);
@@ -334,9 +330,10 @@ int gx_shard_begin(gx_shard* s, int32_t owns_initial, int32_t detect_deadlocks, 
     return GX_OK;
 }
 
-int gx_shard_expand(gx_shard* s) {
+// Level arguments fixed for the whole level (its chunks append to the same
+// next frontier); set by the first expand of a level.
+static void level_args(gx_shard* s) {
     gx_table* t = s->t;
-    const uint32_t v = t->d.vlen;
     LevelArgs& A = s->A;
     A.front = s->F;
     A.nfront = s->nF;
@@ -353,10 +350,21 @@ int gx_shard_expand(gx_shard* s) {
     A.cache_mask = s->cslots ? s->cslots - 1 : 0;
     A.gfilter_mask = s->gslots ? (uint32_t)(s->gslots - 1) : 0;
     A.gfilter = (unsigned long long*)s->gf.p;
-    (void)v;
+    s->level_open = true;
+}
+
+int gx_shard_expand_range(gx_shard* s, uint64_t begin, uint64_t count) {
+    gx_table* t = s->t;
+    const uint32_t v = t->d.vlen;
+    if (!s->level_open) level_args(s);
+    if (begin > s->nF) begin = s->nF;
+    if (count > s->nF - begin) count = s->nF - begin;
+    LevelArgs A = s->A;
+    A.front = s->F + begin * v;
+    A.nfront = count;
     GX_CUDA(cudaEventRecord(s->e0, s->stream));
-    if (s->nF) {
-        const uint64_t want = (s->nF + 31) / 32;
+    if (count) {
+        const uint64_t want = (count + 31) / 32;
         const int g = (int)std::min<uint64_t>((uint64_t)sm_count() * GX_STAGED_MINB, (want + 7) / 8);
         s->K.a<<<g, 256, s->smem, s->stream>>>(t->d, s->n->d, A, s->R);
         GX_LAUNCHED();
@@ -365,31 +373,45 @@ int gx_shard_expand(gx_shard* s) {
     return GX_OK;
 }
 
-int gx_shard_absorb(gx_shard* s, uint64_t* stats) {
+int gx_shard_expand(gx_shard* s) { return gx_shard_expand_range(s, 0, ~0ull); }
+
+int gx_shard_frontier(const gx_shard* s, uint64_t* n) {
+    *n = s->nF;
+    return GX_OK;
+}
+
+int gx_shard_absorb_chunk(gx_shard* s) {
     gx_table* t = s->t;
-    const uint32_t v = t->d.vlen;
     cudaStream_t st = s->stream;
+    if (!s->level_open) level_args(s);
     // the inbox fill is only known on the device: a persistent grid that
     // exits at once when nothing arrived
     GX_CUDA(cudaEventRecord(s->e2, st));
-    int bpm = 0;  // resident absorb blocks per SM
-    GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpm, s->K.b, 128, s->K.absorb_smem));
-    s->K.b<<<sm_count() * std::max(bpm, 1), 128, s->K.absorb_smem, st>>>(t->d, s->A, s->R.inbox[s->rank],
-                                                                        s->R.inbox_ctr[s->rank], s->inbox_cap);
+    s->K.b<<<sm_count() * GX_STAGED_MINB, 256, s->smem, st>>>(t->d, s->A, s->R.inbox[s->rank],
+                                                             s->R.inbox_ctr[s->rank], s->inbox_cap);
     GX_LAUNCHED();
     GX_CUDA(cudaEventRecord(s->e3, st));
-    unsigned long long* hc = (unsigned long long*)t->h_ctr;
     unsigned long long inbox_n = 0;
-    GX_CUDA(cudaMemcpyAsync(hc, t->d_ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaMemcpyAsync(&inbox_n, s->R.inbox_ctr[s->rank], 8, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaMemsetAsync(s->R.inbox_ctr[s->rank], 0, 8, st));
     GX_CUDA(cudaStreamSynchronize(st));
+    if (inbox_n > s->inbox_cap) s->inbox_overflow = true;
     // device time of this shard's two kernels (other shards' kernels may run
     // between them on a shared stream)
     float ma = 0, mb = 0;
     GX_CUDA(cudaEventElapsedTime(&ma, s->e0, s->e1));
     GX_CUDA(cudaEventElapsedTime(&mb, s->e2, s->e3));
     s->level_ms += ma + mb;
+    return GX_OK;
+}
+
+int gx_shard_end_level(gx_shard* s, uint64_t* stats) {
+    gx_table* t = s->t;
+    const uint32_t v = t->d.vlen;
+    cudaStream_t st = s->stream;
+    unsigned long long* hc = (unsigned long long*)t->h_ctr;
+    GX_CUDA(cudaMemcpyAsync(hc, t->d_ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
     const uint64_t claims = s->nF;
     const uint64_t nnew = hc[LV_NEW] - s->new_base;
     s->new_base = hc[LV_NEW];
@@ -408,16 +430,23 @@ int gx_shard_absorb(gx_shard* s, uint64_t* stats) {
     s->F = Fn;
     s->nF = nnew;
     s->rev ^= 1;
-    // cumulative counters except claims / new (per level)
+    s->level_open = false;
+    // per-level claims / new, then cumulative counters
     stats[GX_SH_CLAIMS] = claims;
     stats[GX_SH_NEW] = nnew;
     stats[GX_SH_TRANSITIONS] = hc[LV_TRANS];
     stats[GX_SH_DEADLOCKS] = hc[LV_DL];
     stats[GX_SH_TABLE_FULL] = hc[LV_FULL] ? 1 : 0;
-    stats[GX_SH_OVERFLOW] = (hc[LV_OVF] || inbox_n > s->inbox_cap) ? 1 : 0;
+    stats[GX_SH_OVERFLOW] = (hc[LV_OVF] || s->inbox_overflow) ? 1 : 0;
     stats[GX_SH_ROUTED] = hc[LV_ROUTED];
     stats[GX_SH_PROBES] = hc[LV_PROBES];
+    s->inbox_overflow = false;
     return GX_OK;
+}
+
+int gx_shard_absorb(gx_shard* s, uint64_t* stats) {
+    int rc = gx_shard_absorb_chunk(s);
+    return rc ? rc : gx_shard_end_level(s, stats);
 }
 
 int gx_shard_finish(gx_shard* s, gx_report* rep, uint32_t* deadlocks) {

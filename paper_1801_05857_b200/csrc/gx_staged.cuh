@@ -110,8 +110,8 @@ __device__ __forceinline__ int probe_lane(const TableDesc& T, const uint32_t* km
     return TABLE_FULL;
 }
 
-// KBX > 0 overrides the batch size (the absorb kernel, which has no
-// expansion to overlap, keeps more buckets in flight per warp)
+// KBX > 0 overrides the batch size (a 128-key absorb batch was tried on the
+// B200: 18% slower than 3 blocks x 8 warps x 32 keys, see profiles/README.md)
 template <int BW, int V, int KBX = 0>
 struct Staged {
     static constexpr int CH = BW / 4;                 // 16-byte chunks per bucket

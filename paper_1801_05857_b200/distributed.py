@@ -179,6 +179,10 @@ class FusedShard:
                                     int(cfg.filter_log2), C.byref(h)))
         self._h = h
         self.init = np.asarray(statevec.pack(self.scheme, net.initial), np.uint32)
+        from .network import max_successors
+        # frontier states per chunk so that no inbox can overflow even if every
+        # successor of every sender's chunk went to one owner
+        self.chunk_states = max(1, inbox_capacity // (world * max_successors(net)))
 
     @property
     def handle(self):
@@ -214,6 +218,26 @@ class FusedShard:
     def expand(self):
         from ._lib import check, lib
         check(lib().gx_shard_expand(self._h))
+
+    def frontier(self) -> int:
+        from ._lib import check, lib
+        n = C.c_uint64()
+        check(lib().gx_shard_frontier(self._h, C.byref(n)))
+        return n.value
+
+    def expand_range(self, begin: int, count: int):
+        from ._lib import check, lib
+        check(lib().gx_shard_expand_range(self._h, begin, count))
+
+    def absorb_chunk(self):
+        from ._lib import check, lib
+        check(lib().gx_shard_absorb_chunk(self._h))
+
+    def end_level(self) -> np.ndarray:
+        from ._lib import check, lib, ptr
+        st = np.zeros(8, np.uint64)
+        check(lib().gx_shard_end_level(self._h, ptr(st, C.c_uint64)))
+        return st
 
     def absorb(self) -> np.ndarray:
         from ._lib import check, lib, ptr
@@ -253,28 +277,40 @@ def connect_local(shards):
     check(lib().gx_shard_connect_local(arr, len(shards)))
 
 
-def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None):
+def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None, reduce_max=None):
     """The level protocol shared by the in-process and multi-process
-    drivers: every shard expands, a barrier, every shard absorbs, the
-    level's stats are reduced over all ranks (explore.py:251-265)."""
+    drivers (explore.py:251-265 semantics).  A level is expanded in
+    frontier chunks small enough that no inbox can overflow: for each chunk
+    every shard expands, a barrier, every shard absorbs (and a barrier
+    before the next chunk's peer stores); then the level's stats are
+    reduced over all ranks."""
+    reduce_max = reduce_max or (lambda a: a)
     full = reduce(np.array([sum(int(s.begin(detect)) for s in shards)], np.uint64))[0]
+    chunk = min(s.chunk_states for s in shards)
     rounds = 0
     outcome = "COMPLETE"
     if full:
         outcome = "TABLE_FULL"
     else:
         while True:
-            for s in shards:
-                s.expand()
-            barrier()
+            widest = int(reduce_max(np.array([max(s.frontier() for s in shards)], np.uint64))[0])
+            chunks = max(1, -(-widest // chunk))
+            for c in range(chunks):
+                for s in shards:
+                    s.expand_range(c * chunk, chunk)
+                barrier()
+                for s in shards:
+                    s.absorb_chunk()
+                if c + 1 < chunks:
+                    barrier()
             st = np.zeros(8, np.uint64)
             for s in shards:
-                st += s.absorb()
+                st += s.end_level()
             st = reduce(st)
             rounds += 1
             if st[GX_SH["overflow"]]:
-                raise RuntimeError("frontier or inbox capacity exceeded in sharded exploration; "
-                                   "raise frontier_capacity / inbox_capacity")
+                raise RuntimeError("frontier capacity exceeded in sharded exploration; "
+                                   "raise frontier_capacity")
             if st[GX_SH["table_full"]]:
                 outcome = "TABLE_FULL"
                 break
@@ -363,12 +399,13 @@ def explore_fused(shard: FusedShard, dist, torch, detect: bool, max_iterations=N
     def barrier():
         dist.all_reduce(flag)
 
-    def reduce(a):
+    def reduce(a, op=None):
         t = torch.from_numpy(a.astype(np.int64)).to(dev)
-        dist.all_reduce(t)
+        dist.all_reduce(t, op=op or dist.ReduceOp.SUM)
         return t.cpu().numpy().astype(np.uint64)
 
-    tot, kept, rounds, outcome, _ = _run_levels([shard], barrier, reduce, detect, max_iterations)
+    tot, kept, rounds, outcome, _ = _run_levels([shard], barrier, reduce, detect, max_iterations,
+                                                reduce_max=lambda a: reduce(a, dist.ReduceOp.MAX))
     tot = reduce(tot)
     gathered = [None] * dist.get_world_size()
     dist.all_gather_object(gathered, kept)

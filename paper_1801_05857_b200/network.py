@@ -61,6 +61,22 @@ class Network:
         return self.actions.index(name) if name in self.actions else None
 
 
+def max_successors(net: Network) -> int:
+    """An upper bound on the successors of any composite state: every
+    process's largest independent-move list plus every enabled rule's
+    largest cartesian product (network.py expand() semantics).  Sizes the
+    sharded engine's frontier chunks so no inbox can overflow."""
+    bound = sum(max((len(m) for m in per), default=0) for per in net.indep_moves)
+    for moves in net.rule_moves:
+        if moves is None:
+            continue
+        prod = 1
+        for _proc, per_state in moves:
+            prod *= max((len(d) for d in per_state), default=0)
+        bound += prod
+    return max(bound, 1)
+
+
 def build_network(desc: NetworkDescription, ltss) -> Network:
     ltss = tuple(ltss)
     n = len(ltss)

@@ -161,16 +161,18 @@ def test_sharded_iteration_cap_and_table_full():
 # ------------------------------------------------ fused (peer-routed) driver
 
 class OracleFusedShard:
-    """CPU stand-in for FusedShard (tests only).  expand() probes the
-    locally owned successors at once and stages the others per owner, as
-    k_level_routed does; the P2P inbox stores are emulated by a gloo
-    all_to_all inside absorb() (the device writes them during expand)."""
+    """CPU stand-in for FusedShard (tests only).  expand_range() probes the
+    locally owned successors of a frontier chunk at once and stages the
+    others per owner, as k_level_routed does; the P2P inbox stores are
+    emulated by a gloo all_to_all inside absorb_chunk() (the device writes
+    them during the expansion).  chunk_states is small on purpose, so the
+    driver's chunked levels are exercised."""
 
-    def __init__(self, path, table_kw, world, rank):
+    def __init__(self, path, table_kw, world, rank, chunk_states=7):
         self.base = OracleShard(path, table_kw, world)
         self.rank, self.world = rank, world
         self.vlen = self.base.vlen
-        self.init = None
+        self.chunk_states = chunk_states
 
     def begin(self, detect):
         from paper_1801_05857_b200 import statevec
@@ -181,6 +183,7 @@ class OracleFusedShard:
         self.kept = []
         self.states = 0
         self.front = np.zeros((0, self.vlen), np.uint32)
+        self._level_reset()
         init = np.asarray(statevec.pack(b.scheme, b.net.initial), np.uint32)
         if int(b.owner(init)[0]) == self.rank:
             code, _ = b.table.find_or_insert(init)
@@ -190,12 +193,18 @@ class OracleFusedShard:
             self.states = 1
         return False
 
-    def expand(self):
+    def _level_reset(self):
+        self.next, self.full, self.outgoing = [], False, []
+
+    def frontier(self):
+        return len(self.front)
+
+    def expand_range(self, begin, count):
         b = self.base
-        self.claims = len(self.front)
-        self.expanded += self.claims
+        rows = self.front[begin:begin + count]
+        self.expanded += len(rows)
         succ = []
-        for row in self.front:
+        for row in rows:
             out, c = b.net.expand(b.net.unpack(row))
             self.trans += c
             if not out and self.detect:
@@ -205,12 +214,13 @@ class OracleFusedShard:
         arr = np.array(succ, np.uint32).reshape(-1, self.vlen)
         own = b.owner(arr) if len(arr) else np.zeros(0, np.int64)
         local = arr[own == self.rank]
-        codes, _ = b.table.find_or_insert_batch(local) if len(local) else (np.zeros(0), None)
-        self.next = [local[codes == 1]]
-        self.full = bool((codes == 2).any())
+        if len(local):
+            codes, _ = b.table.find_or_insert_batch(local)
+            self.next.append(local[codes == 1])
+            self.full |= bool((codes == 2).any())
         self.outgoing = [arr[own == r] for r in range(self.world)]
 
-    def absorb(self):
+    def absorb_chunk(self):
         b = self.base
         counts = torch.tensor([len(x) if r != self.rank else 0 for r, x in enumerate(self.outgoing)],
                               dtype=torch.int64)
@@ -227,11 +237,17 @@ class OracleFusedShard:
             codes, _ = b.table.find_or_insert_batch(keys)
             self.next.append(keys[codes == 1])
             self.full |= bool((codes == 2).any())
-        self.front = np.concatenate(self.next).reshape(-1, self.vlen)
+        self.outgoing = [np.zeros((0, self.vlen), np.uint32)] * self.world
+
+    def end_level(self):
+        claims = len(self.front)
+        self.front = np.concatenate(self.next).reshape(-1, self.vlen) if self.next else \
+            np.zeros((0, self.vlen), np.uint32)
         self.states += len(self.front)
         st = np.zeros(8, np.uint64)
-        st[0], st[1], st[2], st[3], st[4] = self.claims, len(self.front), self.trans, self.dl_total, \
+        st[0], st[1], st[2], st[3], st[4] = claims, len(self.front), self.trans, self.dl_total, \
             int(self.full)
+        self._level_reset()
         return st
 
     def finish(self):
