@@ -65,7 +65,7 @@ def parse():
                     help="one table, or hash-owner shards on this GPU (auto: shards once one "
                          "table would outgrow the TLB reach)")
     ap.add_argument("--shards", type=int, default=0, help="shard count (0 = auto)")
-    ap.add_argument("--inbox-frac", type=float, default=0.12,
+    ap.add_argument("--inbox-frac", type=float, default=0.18,
                     help="sharded engine: inbox keys per shard = frac * states / shards")
     ap.add_argument("--frontier-frac", type=float, default=0.035,
                     help="frontier vectors per shard = frac * states / shards")

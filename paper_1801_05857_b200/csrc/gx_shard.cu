@@ -54,7 +54,9 @@ __global__ void __launch_bounds__(256, GX_STAGED_MINB) k_absorb(TableDesc T, Lev
         for (uint32_t i = threadIdx.x; i <= cmask; i += blockDim.x) dcache[i] = 0ull;
         __syncthreads();
     }
-    const uint64_t n = min((uint64_t)*count, cap);
+    const uint64_t sent = *count;
+    if (sent > cap && blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&A.ctr[LV_OVF], 1ull);
+    const uint64_t n = min(sent, cap);
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
     unsigned long long probes = 0;
@@ -138,11 +140,13 @@ struct gx_shard {
     uint64_t n_pending = 0;
     LevelArgs A;
     std::vector<uint32_t> kept, dlhost;
-    cudaEvent_t e0, e1, e2, e3;  // kernel A: e0..e1, kernel B: e2..e3
+    // CUDA-event pairs around each kernel of the current level (A and B of
+    // every chunk), read once at the end of the level
+    std::vector<cudaEvent_t> ev;
+    size_t ev_used = 0;
     double level_ms = 0;
     int32_t detect = 0;
-    bool level_open = false;      // LevelArgs of the current level are set
-    bool inbox_overflow = false;  // some chunk overflowed the inbox
+    bool level_open = false;  // LevelArgs of the current level are set
 };
 
 extern "C" {
@@ -212,10 +216,6 @@ int gx_shard_create(gx_net* n, gx_table* t, int32_t rank, int32_t world, uint64_
     GX_CUDA(cudaMemsetAsync(s->inbox_block, 0, INBOX_HEAD, s->stream));
     GX_CUDA(cudaFuncSetAttribute((const void*)K.a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem));
     GX_CUDA(cudaFuncSetAttribute((const void*)K.b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem));
-    GX_CUDA(cudaEventCreate(&s->e0));
-    GX_CUDA(cudaEventCreate(&s->e1));
-    GX_CUDA(cudaEventCreate(&s->e2));
-    GX_CUDA(cudaEventCreate(&s->e3));
     *out = s;
     return GX_OK;
 }
@@ -228,10 +228,7 @@ int gx_shard_destroy(gx_shard* s) {
     s->fb.release();
     s->dl.release();
     s->gf.release();
-    cudaEventDestroy(s->e0);
-    cudaEventDestroy(s->e1);
-    cudaEventDestroy(s->e2);
-    cudaEventDestroy(s->e3);
+    for (cudaEvent_t e : s->ev) cudaEventDestroy(e);
     delete s;
     return GX_OK;
 }
@@ -305,7 +302,7 @@ int gx_shard_begin(gx_shard* s, int32_t owns_initial, int32_t detect_deadlocks, 
     s->level_ms = 0;
     s->detect = detect_deadlocks;
     s->level_open = false;
-    s->inbox_overflow = false;
+    s->ev_used = 0;
     *table_full = 0;
     if (owns_initial) {
         rc = t->codes.ensure(16);
@@ -328,6 +325,15 @@ int gx_shard_begin(gx_shard* s, int32_t owns_initial, int32_t detect_deadlocks, 
     }
     // the level counters restart from zero (the table clear zeroed them)
     return GX_OK;
+}
+
+static cudaEvent_t next_event(gx_shard* s) {
+    if (s->ev_used == s->ev.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        s->ev.push_back(e);
+    }
+    return s->ev[s->ev_used++];
 }
 
 // Level arguments fixed for the whole level (its chunks append to the same
@@ -362,14 +368,15 @@ int gx_shard_expand_range(gx_shard* s, uint64_t begin, uint64_t count) {
     LevelArgs A = s->A;
     A.front = s->F + begin * v;
     A.nfront = count;
-    GX_CUDA(cudaEventRecord(s->e0, s->stream));
+    cudaEvent_t a0 = next_event(s), a1 = next_event(s);
+    GX_CUDA(cudaEventRecord(a0, s->stream));
     if (count) {
         const uint64_t want = (count + 31) / 32;
         const int g = (int)std::min<uint64_t>((uint64_t)sm_count() * GX_STAGED_MINB, (want + 7) / 8);
         s->K.a<<<g, 256, s->smem, s->stream>>>(t->d, s->n->d, A, s->R);
         GX_LAUNCHED();
     }
-    GX_CUDA(cudaEventRecord(s->e1, s->stream));
+    GX_CUDA(cudaEventRecord(a1, s->stream));
     return GX_OK;
 }
 
@@ -384,24 +391,16 @@ int gx_shard_absorb_chunk(gx_shard* s) {
     gx_table* t = s->t;
     cudaStream_t st = s->stream;
     if (!s->level_open) level_args(s);
-    // the inbox fill is only known on the device: a persistent grid that
-    // exits at once when nothing arrived
-    GX_CUDA(cudaEventRecord(s->e2, st));
+    // asynchronous: the inbox fill is only known on the device (a
+    // persistent grid exits at once when nothing arrived, and flags an
+    // overflowing inbox in LV_OVF); the counter is reset in stream order
+    cudaEvent_t b0 = next_event(s), b1 = next_event(s);
+    GX_CUDA(cudaEventRecord(b0, st));
     s->K.b<<<sm_count() * GX_STAGED_MINB, 256, s->smem, st>>>(t->d, s->A, s->R.inbox[s->rank],
                                                              s->R.inbox_ctr[s->rank], s->inbox_cap);
     GX_LAUNCHED();
-    GX_CUDA(cudaEventRecord(s->e3, st));
-    unsigned long long inbox_n = 0;
-    GX_CUDA(cudaMemcpyAsync(&inbox_n, s->R.inbox_ctr[s->rank], 8, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaEventRecord(b1, st));
     GX_CUDA(cudaMemsetAsync(s->R.inbox_ctr[s->rank], 0, 8, st));
-    GX_CUDA(cudaStreamSynchronize(st));
-    if (inbox_n > s->inbox_cap) s->inbox_overflow = true;
-    // device time of this shard's two kernels (other shards' kernels may run
-    // between them on a shared stream)
-    float ma = 0, mb = 0;
-    GX_CUDA(cudaEventElapsedTime(&ma, s->e0, s->e1));
-    GX_CUDA(cudaEventElapsedTime(&mb, s->e2, s->e3));
-    s->level_ms += ma + mb;
     return GX_OK;
 }
 
@@ -412,6 +411,14 @@ int gx_shard_end_level(gx_shard* s, uint64_t* stats) {
     unsigned long long* hc = (unsigned long long*)t->h_ctr;
     GX_CUDA(cudaMemcpyAsync(hc, t->d_ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaStreamSynchronize(st));
+    // device time of this shard's kernels (other shards' kernels may run
+    // between them on a shared stream, so pairs are timed one by one)
+    for (size_t i = 0; i + 1 < s->ev_used; i += 2) {
+        float ms = 0;
+        GX_CUDA(cudaEventElapsedTime(&ms, s->ev[i], s->ev[i + 1]));
+        s->level_ms += ms;
+    }
+    s->ev_used = 0;
     const uint64_t claims = s->nF;
     const uint64_t nnew = hc[LV_NEW] - s->new_base;
     s->new_base = hc[LV_NEW];
@@ -437,10 +444,9 @@ int gx_shard_end_level(gx_shard* s, uint64_t* stats) {
     stats[GX_SH_TRANSITIONS] = hc[LV_TRANS];
     stats[GX_SH_DEADLOCKS] = hc[LV_DL];
     stats[GX_SH_TABLE_FULL] = hc[LV_FULL] ? 1 : 0;
-    stats[GX_SH_OVERFLOW] = (hc[LV_OVF] || s->inbox_overflow) ? 1 : 0;
+    stats[GX_SH_OVERFLOW] = hc[LV_OVF] ? 1 : 0;
     stats[GX_SH_ROUTED] = hc[LV_ROUTED];
     stats[GX_SH_PROBES] = hc[LV_PROBES];
-    s->inbox_overflow = false;
     return GX_OK;
 }
 

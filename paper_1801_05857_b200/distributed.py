@@ -518,10 +518,17 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, cl
                         cache_slots=max(1, args.cache_slots))
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream().cuda_stream
-    frontier = max(1 << 20, per_rank // 6)
+    # frontier: two adjacent levels of this rank with margin; inbox: most of
+    # what is left after the table, so that levels need few chunks
+    frontier = max(1 << 20, per_rank // 12)
+    free = torch.cuda.mem_get_info()[0]
+    if torch.cuda.device_count() < world:  # ranks sharing a GPU (functional check)
+        free //= world
+    table_b = cap_words * 4 * 9 // 8  # data + status bytes (bw 32)
+    inbox = max(1 << 20, int((free - table_b - frontier * 4 * vlen) * 0.7) // (4 * vlen))
 
     def make():
-        sh = FusedShard(net, cfg, rank, world, inbox_capacity=frontier, frontier_capacity=frontier,
+        sh = FusedShard(net, cfg, rank, world, inbox_capacity=inbox, frontier_capacity=frontier,
                         stream=stream)
         connect_fused(sh, dist)
         return sh
