@@ -257,8 +257,11 @@ int gx_shard_create(gx_net *n, gx_table *t, int32_t rank, int32_t world, uint64_
 int gx_shard_destroy(gx_shard *s);
 /* CUDA IPC handle of this shard's inbox (GX_IPC_HANDLE_BYTES bytes) */
 int gx_shard_ipc_handle(gx_shard *s, uint8_t *out);
-/* map every peer's inbox (world handles, rank order; own entry ignored) */
+/* map every peer's inbox (world handles, rank order; own entry ignored;
+ * an all-zero handle marks a peer in this process: gx_shard_link it) */
 int gx_shard_connect(gx_shard *s, const uint8_t *handles);
+/* point s at the inbox of a peer shard living in the same process */
+int gx_shard_link(gx_shard *s, const gx_shard *peer);
 /* all shards of one process (one GPU or several): connect them directly */
 int gx_shard_connect_local(gx_shard *const *shards, int32_t world);
 /* clear the shard's table; insert the initial state if this rank owns it */

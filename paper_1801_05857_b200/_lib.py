@@ -98,6 +98,7 @@ SIGNATURES = {
     "gx_shard_ipc_handle": (C.c_int, [_vp, _u8p]),
     "gx_shard_connect": (C.c_int, [_vp, _u8p]),
     "gx_shard_connect_local": (C.c_int, [_P(_vp), C.c_int32]),
+    "gx_shard_link": (C.c_int, [_vp, _vp]),
     "gx_shard_begin": (C.c_int, [_vp, C.c_int32, C.c_int32, _i32p]),
     "gx_shard_expand": (C.c_int, [_vp]),
     "gx_shard_absorb": (C.c_int, [_vp, _u64p]),

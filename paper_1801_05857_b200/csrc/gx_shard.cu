@@ -248,19 +248,40 @@ static void set_peer(gx_shard* s, int r, void* block) {
 }
 
 int gx_shard_connect(gx_shard* s, const uint8_t* handles) {
+    static const uint8_t zero[GX_IPC_HANDLE_BYTES] = {};
     for (int r = 0; r < s->world; r++) {
         if (r == s->rank) {
             set_peer(s, r, s->inbox_block);
             continue;
         }
+        const uint8_t* hb = handles + (size_t)r * GX_IPC_HANDLE_BYTES;
+        if (!memcmp(hb, zero, GX_IPC_HANDLE_BYTES)) continue;  // same-process peer: gx_shard_link
         cudaIpcMemHandle_t h;
-        memcpy(&h, handles + (size_t)r * GX_IPC_HANDLE_BYTES, sizeof h);
+        memcpy(&h, hb, sizeof h);
         void* p = nullptr;
         GX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
         s->opened.push_back(p);
         set_peer(s, r, p);
     }
+    for (int r = 0; r < s->world; r++)
+        if (!s->R.inbox[r]) {
+            s->connected = false;
+            return GX_OK;  // waiting for gx_shard_link of the same-process peers
+        }
     s->connected = true;
+    return GX_OK;
+}
+
+int gx_shard_link(gx_shard* s, const gx_shard* peer) {
+    if (peer->world != s->world || peer->inbox_cap != s->inbox_cap) {
+        set_error("link: peer shard has world %d / inbox %llu, this one %d / %llu", peer->world,
+                  (unsigned long long)peer->inbox_cap, s->world, (unsigned long long)s->inbox_cap);
+        return GX_EINPUT;
+    }
+    set_peer(s, peer->rank, peer->inbox_block);
+    bool all = true;
+    for (int r = 0; r < s->world; r++) all = all && s->R.inbox[r] != nullptr;
+    s->connected = all;
     return GX_OK;
 }
 

@@ -145,6 +145,7 @@ class DeviceShard:
 GX_SH = dict(claims=0, new=1, transitions=2, deadlocks=3, table_full=4, overflow=5, routed=6,
              probes=7)
 IPC_HANDLE_BYTES = 64
+IPC_ZERO = bytes(IPC_HANDLE_BYTES)  # "same-process peer" in gx_shard_connect
 
 
 class FusedShard:
@@ -388,11 +389,14 @@ def explore_local_shards(net, cfg, world: int, inbox_capacity: int = 0, frontier
         ex.close()
 
 
-def explore_fused(shard: FusedShard, dist, torch, detect: bool, max_iterations=None,
+def explore_fused(shards, dist, torch, detect: bool, max_iterations=None,
                   device=None) -> ShardResult:
-    """Multi-process driver (one process per GPU): shards were connected
-    with their peers' IPC handles; the barrier and the stats reduction are
-    NCCL all_reduces on the shards' stream."""
+    """Multi-process driver (one process per GPU, holding one shard or
+    several): shards were connected with their peers' IPC handles; the
+    barrier and the stats reductions are NCCL all_reduces on the shards'
+    stream."""
+    if not isinstance(shards, (list, tuple)):
+        shards = [shards]
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     flag = torch.zeros(1, dtype=torch.int64, device=dev)
 
@@ -404,7 +408,7 @@ def explore_fused(shard: FusedShard, dist, torch, detect: bool, max_iterations=N
         dist.all_reduce(t, op=op or dist.ReduceOp.SUM)
         return t.cpu().numpy().astype(np.uint64)
 
-    tot, kept, rounds, outcome, _ = _run_levels([shard], barrier, reduce, detect, max_iterations,
+    tot, kept, rounds, outcome, _ = _run_levels(list(shards), barrier, reduce, detect, max_iterations,
                                                 reduce_max=lambda a: reduce(a, dist.ReduceOp.MAX))
     tot = reduce(tot)
     gathered = [None] * dist.get_world_size()
@@ -415,11 +419,25 @@ def explore_fused(shard: FusedShard, dist, torch, detect: bool, max_iterations=N
                        outcome=outcome, levels=rounds - 1)
 
 
-def connect_fused(shard: FusedShard, dist):
-    """Exchange the shards' inbox IPC handles and map the peers'."""
-    handles = [None] * dist.get_world_size()
-    dist.all_gather_object(handles, shard.ipc_handle())
-    shard.connect(handles)
+def connect_fused(shards, dist):
+    """Exchange the shards' inbox IPC handles and map the peers': shards in
+    other processes through CUDA IPC, shards of this process directly."""
+    from ._lib import check, lib
+    if not isinstance(shards, (list, tuple)):
+        shards = [shards]
+    mine = {s.rank: s.ipc_handle() for s in shards}
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, mine)
+    world = shards[0].world
+    table = [IPC_ZERO] * world
+    for part in parts:
+        for r, h in part.items():
+            table[r] = h
+    for s in shards:
+        s.connect([IPC_ZERO if r in mine else table[r] for r in range(world)])
+        for p in shards:
+            if p is not s:
+                check(lib().gx_shard_link(s.handle, p.handle))
 
 
 def explore_sharded(backend, dist, torch, scheme, initial_packed: np.ndarray, detect: bool,
@@ -510,28 +528,41 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, cl
     scheme = statevec.make_scheme(net)
     vlen = scheme.vector_length
     cf = closed_form(args.workload)
-    per_rank = cf[0] // world + (cf[0] >> 8) + 4096
-    cap_words = table_capacity(per_rank, vlen, args.bucket_words, args.load)
+    # shards per GPU: enough that each table stays inside the TLB reach
+    # (profiles/README.md); global shard id = rank * local + l
+    per_gpu = cf[0] // world
+    gpu_bytes = table_capacity(per_gpu, vlen, args.bucket_words, args.load) * 4
+    local = args.shards or max(1, -(-gpu_bytes // (40 << 30)))
+    gworld = world * local
+    per_shard = cf[0] // gworld + (cf[0] >> 8) // gworld + 4096
+    cap_words = table_capacity(per_shard, vlen, args.bucket_words, args.load)
     cfg = ExploreConfig(table=TableConfig(bucket_words=args.bucket_words,
                                           num_hash_functions=args.hash_functions,
                                           capacity_words=cap_words), detect_deadlocks=True,
                         cache_slots=max(1, args.cache_slots))
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream().cuda_stream
-    # frontier: two adjacent levels of this rank with margin; inbox: most of
-    # what is left after the table, so that levels need few chunks
-    frontier = max(1 << 20, per_rank // 12)
+    # frontier: two adjacent levels with margin; inbox: most of what is left
+    # after the tables, so that levels need few chunks
+    frontier = max(1 << 20, int(per_shard * 0.05))
     free = torch.cuda.mem_get_info()[0]
     if torch.cuda.device_count() < world:  # ranks sharing a GPU (functional check)
         free //= world
-    table_b = cap_words * 4 * 9 // 8  # data + status bytes (bw 32)
-    inbox = max(1 << 20, int((free - table_b - frontier * 4 * vlen) * 0.7) // (4 * vlen))
+    table_b = cap_words * 4 * local  # data; the status array is dropped when it does not fit
+    status = table_b * 9 // 8 + 0.3 * (free - table_b) < free
+    table_b = table_b * 9 // 8 if status else table_b
+    inbox = max(1 << 20, int((free - table_b - local * frontier * 4 * vlen) * 0.7) // (4 * vlen * local))
 
     def make():
-        sh = FusedShard(net, cfg, rank, world, inbox_capacity=inbox, frontier_capacity=frontier,
-                        stream=stream)
-        connect_fused(sh, dist)
-        return sh
+        shards = [FusedShard(net, cfg, rank * local + l, gworld, inbox_capacity=inbox,
+                             frontier_capacity=frontier, stream=stream, status=status)
+                  for l in range(local)]
+        connect_fused(shards, dist)
+        return shards
+
+    def close(shards):
+        for sh in shards:
+            sh.close()
 
     shard = make()
     res = None
@@ -554,7 +585,7 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, cl
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
-    shard.close()
+    close(shard)
     assert (res.states, res.transitions) == cf, (res.states, res.transitions, cf)
     # e2e: shards built (CSR from host memory, tables, inboxes, IPC) every step
     e2e = []
@@ -563,7 +594,7 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, cl
         t0 = time.perf_counter()
         sh = make()
         r = explore_fused(sh, dist, torch, True, device=dev)
-        sh.close()
+        close(sh)
         torch.cuda.synchronize()
         t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -578,12 +609,14 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, cl
         "config": {"workload": f"configs[4] token ring N={args.workload[4:]} hash-partitioned",
                    "states": res.states, "transitions": res.transitions, "levels": res.levels,
                    "vector_words": vlen, "bucket_words": args.bucket_words,
-                   "hash_functions": args.hash_functions, "table_words_per_rank": cap_words,
+                   "hash_functions": args.hash_functions, "table_words_per_shard": cap_words,
+                   "shards_per_gpu": local, "status_array": bool(status),
                    "block_cache_slots": args.cache_slots,
                    "l2_policy": "tables re-zeroed every step; tables >> 126 MB L2",
-                   "parallelism": f"hash-owner sharding x{world}: successors routed to the owner's "
-                                  "inbox by P2P stores inside the level kernel (CUDA IPC over "
-                                  "NVLink), NCCL all_reduce of level counters"},
+                   "parallelism": f"hash-owner sharding x{gworld} ({local} per GPU): successors "
+                                  "routed to the owner's inbox by P2P stores inside the level "
+                                  "kernel (CUDA IPC over NVLink), NCCL all_reduce of level "
+                                  "counters"},
         "roofline": None, "cpu_baseline": None,
         "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": None,
                 "d2h_bytes_per_step": None,

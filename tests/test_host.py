@@ -102,14 +102,19 @@ def test_fig_independent_sets():
 def test_host_expand_matches_reference_kats():
     """Point-query expand (API compatibility) equals the reference's expand
     on every reachable state of the small golden models, order included."""
+    from paper_1801_05857_b200.network import max_successors
     kats = json.loads((GOLDEN / "expand_kats.json").read_text())
     warnings.simplefilter("ignore")
     for name, rows in kats.items():
         net = load_network(model_path(name))
+        # network.max_successors sizes the sharded engine's frontier chunks
+        # (no inbox may overflow): it must bound every reachable state
+        bound = max_successors(net)
         for s, count, succ in rows:
             got, c = expand(net, tuple(s))
             assert c == count, (name, s)
             assert [[net.actions[a], list(t)] for a, t in got] == succ, (name, s)
+            assert len(succ) <= bound, (name, s)
 
 
 def test_golden_errors_reproduced():
@@ -203,3 +208,4 @@ def test_cli_gen_model_and_input_errors(tmp_path, capsys):
     assert main(["explore", str(tmp_path / "r3" / "net.exp"), "--oracle"]) == 1
     assert main(["explore", "--bucket-size", "5", "x"]) == 1
     assert main(["nonsense"]) == 1
+
