@@ -420,7 +420,9 @@ def main():
     traffic = None
     if TRAFFIC.exists():
         tr = json.loads(TRAFFIC.read_text())
-        traffic = tr.get(f"{args.workload}/bw{args.bucket_words}")
+        key = f"{args.workload}/bw{args.bucket_words}/shards{shards}"
+        if key in tr:  # DRAM bytes of one exploration's level kernels (ncu, profiles/)
+            traffic = tr[key]["bytes_per_step"]
     ex.close()
 
     # the random-access roofline R(g) on this GPU: a 32 GiB buffer (>> L2,
