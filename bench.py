@@ -81,6 +81,8 @@ def parse():
     ap.add_argument("--no-hash-bench", action="store_true",
                     help="skip the isolated hash-table sweeps (configs[1])")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the configs[2] (peterson6) and ring16 side measurements")
     return ap.parse_args()
 
 
@@ -289,6 +291,37 @@ def duplication_sweep(ra: dict):
             out.append({"bw": bw, "d": d, "ops_per_sec": r["ops_per_sec"], "inserted": r["inserted"],
                         "found": r["found"], "gbs_alg": alg,
                         "frac_of_random_roofline": alg / r_g if r_g else None})
+    return out
+
+
+def extra_workloads(torch, tmp: Path):
+    """Side measurements on one table (not the headline): configs[2], a
+    peterson7-class model (Peterson's filter lock with 6 processes, ~1e8
+    states), and ring16 (8 GB table), each 1 warm-up + 2 timed runs."""
+    import paper_1801_05857_b200 as gx
+    from paper_1801_05857_b200.explore import ExploreConfig, Explorer
+    from paper_1801_05857_b200.hashtable import TableConfig
+    out = []
+    for name, words, k in (("peterson6", 1 << 31, 16), ("ring16", table_capacity(459165024, 2, 32, 0.5), 8)):
+        net = gx.load_network(model_path(name, tmp))
+        cfg = ExploreConfig(table=TableConfig(capacity_words=words, num_hash_functions=k),
+                            detect_deadlocks=True)
+        ex = Explorer(net, cfg, stream=torch.cuda.current_stream().cuda_stream)
+        ex.run()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        reps = [ex.run() for _ in range(2)]
+        e1.record()
+        torch.cuda.synchronize()
+        ex.close()
+        r = reps[-1]
+        assert r.outcome == "COMPLETE" and reps[0].states == r.states
+        ms = e0.elapsed_time(e1) / 2
+        out.append({"workload": ("configs[2] " if name.startswith("peterson") else "") + name,
+                    "states": r.states, "transitions": r.transitions, "levels": r.iterations - 1,
+                    "table_bytes": words * 4, "ms_per_exploration": ms,
+                    "states_per_sec": r.states / (ms / 1e3)})
     return out
 
 
@@ -507,6 +540,8 @@ def main():
     }
     if not args.no_hash_bench:
         line["hash_bench"] = {"fill_sweep": hash_sweep(ra), "duplication_sweep": duplication_sweep(ra)}
+    if not args.no_extra:
+        line["extra_workloads"] = extra_workloads(torch, tmp)
     print(json.dumps(line), flush=True)
 
 

@@ -989,7 +989,11 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
         uint64_t nF = 1;
         int rev = 1;
         unsigned long long new_base = 0, dl_base = 0;
-        const int grid = persistent_grid();
+        // exactly the resident blocks: one wave, so every block's strided
+        // share of the frontier runs concurrently (no partial last wave)
+        int resident = 0;
+        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, lk, 256, csmem));
+        const int grid = sm_count() * std::max(resident, 1);
         cudaEvent_t la, lb;
         GX_CUDA(cudaEventCreate(&la));
         GX_CUDA(cudaEventCreate(&lb));
@@ -1277,7 +1281,9 @@ int gx_bench_find_or_put_rows(gx_table* t, uint64_t total, uint64_t dup, uint64_
     GX_CUDA(cudaEventRecord(e0, st));
     if (BK.smem) GX_CUDA(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)BK.smem));
-    k<<<persistent_grid(), 256, BK.smem, st>>>(T, B);
+    int resident = 0;
+    GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k, 256, BK.smem));
+    k<<<sm_count() * std::max(resident, 1), 256, BK.smem, st>>>(T, B);
     GX_LAUNCHED();
     GX_CUDA(cudaEventRecord(e1, st));
     unsigned long long h[2];

@@ -163,8 +163,8 @@ class FusedShard:
 
         self.rank, self.world = rank, world
         self.scheme = statevec.make_scheme(net)
-        self.vlen = self.scheme.vector_length
-        self.dnet = DeviceNetwork(net, self.scheme, stream)
+        self.vlen = statevec.device_vlen(self.scheme, cfg.pad_vlen3)
+        self.dnet = DeviceNetwork(net, self.scheme, stream, self.vlen)
         self.table = StateTable(cfg.table, self.vlen, mark=statevec.mark_bit(self.scheme),
                                 stream=stream, status=status)
         slots = self.table.total_slots
@@ -179,7 +179,9 @@ class FusedShard:
                                     frontier_capacity, int(min(cfg.cache_slots, 1 << 30)),
                                     int(cfg.filter_log2), C.byref(h)))
         self._h = h
-        self.init = np.asarray(statevec.pack(self.scheme, net.initial), np.uint32)
+        self.init = np.zeros(self.vlen, np.uint32)
+        packed = statevec.pack(self.scheme, net.initial)
+        self.init[:len(packed)] = packed
         from .network import max_successors
         # frontier states per chunk so that no inbox can overflow even if every
         # successor of every sender's chunk went to one owner
@@ -252,7 +254,8 @@ class FusedShard:
         rep = Report()
         dl = np.zeros((100, self.vlen), np.uint32)
         check(lib().gx_shard_finish(self._h, C.byref(rep), ptr(dl)))
-        kept = [statevec.unpack(self.scheme, tuple(int(x) for x in dl[i]))
+        sv = self.scheme.vector_length
+        kept = [statevec.unpack(self.scheme, tuple(int(x) for x in dl[i, :sv]))
                 for i in range(rep.deadlocks_kept)]
         return rep, kept
 

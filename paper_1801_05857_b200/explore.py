@@ -55,6 +55,10 @@ class ExploreConfig:
     # the table (0 = off): duplicate successors generated anywhere on the GPU
     # skip their random table probe
     filter_log2: int = 0
+    # store 3-word states padded to 4 words (in-band table, one 128-bit CAS
+    # per insert) instead of the status-byte protocol; the table then has
+    # vlen-4 slots (8 per 32-word bucket instead of 10)
+    pad_vlen3: bool = True
 
     def __post_init__(self):
         if self.workers < 1:
@@ -99,12 +103,15 @@ class ExplorationReport:
 class DeviceNetwork:
     """A Network's CSR uploaded to the device once (gx_net_create)."""
 
-    def __init__(self, net: Network, scheme=None, stream=None):
+    def __init__(self, net: Network, scheme=None, stream=None, vlen: int | None = None):
         self.net = net
         self.scheme = scheme or statevec.make_scheme(net)
-        csr = to_csr(net, self.scheme)
+        self.vlen = vlen or self.scheme.vector_length  # device words per state (padding)
+        csr = to_csr(net, self.scheme, self.vlen)
         self._arrays = csr
-        init = np.asarray(statevec.pack(self.scheme, net.initial), np.uint32)
+        init = np.zeros(self.vlen, np.uint32)
+        packed = statevec.pack(self.scheme, net.initial)
+        init[:len(packed)] = packed
         self._init = init
         c = NetworkCsr()
         c.nproc, c.nrules, c.vlen = csr["nproc"], csr["nrules"], csr["vlen"]
@@ -164,8 +171,9 @@ class Explorer:
         self.net = net
         self.cfg = cfg
         self.scheme = statevec.make_scheme(net)
-        self.dnet = DeviceNetwork(net, self.scheme, stream)
-        self.table = StateTable(cfg.table, self.scheme.vector_length,
+        self.vlen = statevec.device_vlen(self.scheme, cfg.pad_vlen3)
+        self.dnet = DeviceNetwork(net, self.scheme, stream, self.vlen)
+        self.table = StateTable(cfg.table, self.vlen,
                                 mark=statevec.mark_bit(self.scheme), stream=stream, status=status)
         self.last = None
 
@@ -175,13 +183,14 @@ class Explorer:
                           int(cfg.frontier_capacity), int(cfg.probe_group),
                           int(min(cfg.cache_slots, 1 << 30)))
         rep = Report()
-        v = self.scheme.vector_length
+        v = self.vlen
         dl = np.zeros((DEADLOCK_KEEP, v), np.uint32)
         t0 = time.perf_counter()
         check(lib().gx_explore(self.dnet.handle, self.table.handle, C.byref(ecfg), C.byref(rep),
                                ptr(dl)))
         wall = time.perf_counter() - t0
-        kept = [statevec.unpack(self.scheme, tuple(int(x) for x in dl[i]))
+        sv = self.scheme.vector_length
+        kept = [statevec.unpack(self.scheme, tuple(int(x) for x in dl[i, :sv]))
                 for i in range(rep.deadlocks_kept)]
         self.last = rep
         return ExplorationReport(
@@ -193,10 +202,11 @@ class Explorer:
             kernels=int(rep.kernels), level_ms=float(rep.level_ms), probes=int(rep.probes))
 
     def dump_states(self) -> str:
-        return statevec.dump_states_array(self.table.dump_arrays()[2])
+        return statevec.dump_states_array(self.table.dump_arrays()[2][:, :self.scheme.vector_length])
 
     def dump_table(self) -> str:
         hs, st, ws = self.table.dump_arrays()
+        ws = ws[:, :self.scheme.vector_length]
         spb = self.table.slots_per_bucket
         lines = ["bucket,slot,status,words\n"]
         for h, s, w in zip(hs, st, ws):

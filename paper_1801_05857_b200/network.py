@@ -238,7 +238,7 @@ def _may_collide(net: Network, r1: int, r2: int) -> bool:
     return True
 
 
-def to_csr(net: Network, scheme) -> dict:
+def to_csr(net: Network, scheme, vlen: int | None = None) -> dict:
     """Flatten the move tables for the device (layout: include/gx.h,
     gx_network_csr).  Returns u32 numpy arrays."""
     P = len(net.processes)
@@ -297,7 +297,7 @@ def to_csr(net: Network, scheme) -> dict:
 
     u32 = lambda x, w=1: np.ascontiguousarray(np.asarray(x, np.uint32).reshape(-1)) if len(x) else np.zeros(w, np.uint32)
     return {
-        "nproc": P, "nrules": len(enabled), "vlen": scheme.vector_length,
+        "nproc": P, "nrules": len(enabled), "vlen": vlen or scheme.vector_length,
         "proc": u32(proc), "qtab": u32(qtab, 4), "im_dst": u32(im_dst),
         "trig": u32(trig), "rules": u32(rules, 4), "parts": u32(parts, 4),
         "rq": u32(rq, 2), "rdst": u32(rdst), "dedup": u32(dedup),

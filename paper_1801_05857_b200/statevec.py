@@ -106,6 +106,15 @@ def dump_states_array(words: np.ndarray) -> str:
     return "\n".join(lines.tolist()) + "\n"
 
 
+def device_vlen(scheme: PackingScheme, pad: bool = True) -> int:
+    """Words per state on the device: a 3-word state is stored padded to 4
+    words (the padding word is zero), so the exploration table can use the
+    in-band mode with one 128-bit CAS per insert instead of the status-byte
+    protocol.  The state set is unchanged; the table holds vlen-4 slots."""
+    v = scheme.vector_length
+    return 4 if (pad and v == 3) else v
+
+
 def mark_bit(scheme: PackingScheme):
     """(word, bit) of a bit no packed state ever sets -- the top bit of the
     word with the most unused bits -- or None if every word is full."""

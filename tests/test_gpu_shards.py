@@ -101,3 +101,25 @@ def test_sharded_contention(bw, world, tmp_path):
                 (states, 4 * n * n * 3 ** (n - 2), 6 * n - 4 + 1, "COMPLETE")
     finally:
         ex.close()
+
+
+def test_peterson6_single_table_equals_shards(tmp_path):
+    """configs[2] (a peterson7-class model: Peterson's filter lock, 6
+    processes, ~10^8 states) is beyond the CPU oracle, so two independent
+    device engines pin each other: the single-table staged level kernel
+    and the hash-owner sharded engine (routing + absorb) must agree on
+    states, transitions, levels and deadlocks.  Peterson N <= 5 is pinned
+    against the oracle in test_generated_models_match_oracle."""
+    from paper_1801_05857_b200.bench import gen_peterson
+    _, p = gen_peterson(6, tmp_path / "p6")
+    net = gx.load_network(p)
+    cfg = ExploreConfig(table=TableConfig(capacity_words=1 << 31, num_hash_functions=16),
+                        detect_deadlocks=True)
+    one = gx.explore(net, cfg)
+    cfg3 = ExploreConfig(table=TableConfig(capacity_words=(1 << 31) // 3, num_hash_functions=16),
+                         detect_deadlocks=True)
+    three = D.explore_local_shards(net, cfg3, 3)
+    assert one.outcome == three.outcome == "COMPLETE"
+    assert (one.states, one.transitions, one.iterations, one.deadlocks_total) == \
+        (three.states, three.transitions, three.iterations, three.deadlocks_total)
+    assert one.states > 10 ** 8
