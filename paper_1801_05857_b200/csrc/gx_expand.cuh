@@ -26,19 +26,29 @@ __device__ __forceinline__ uint32_t field_get(const uint32_t* s, uint32_t word, 
 template <int V>
 __device__ __forceinline__ bool rule_generates(const NetDesc& N, uint32_t r, const uint32_t* s,
                                                const uint32_t* t) {
-    const uint4 rl = __ldg(&N.rules[r]);
-    uint32_t allowed[V];
+    if (V <= 4 && N.rmask) {
+        // t may differ from s only in r's participants
+        const uint4 m = __ldg(&N.rmask[r]);
+        const uint32_t allowed[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
-    for (int w = 0; w < V; w++) allowed[w] = 0;
-    for (uint32_t k = 0; k < rl.x; k++) {
-        const uint4 pt = __ldg(&N.parts[rl.y + k]);
+        for (int w = 0; w < (V < 4 ? V : 4); w++)
+            if ((s[w] ^ t[w]) & ~allowed[w]) return false;
+    }
+    const uint4 rl = __ldg(&N.rules[r]);
+    if (V > 4 || !N.rmask) {
+        uint32_t allowed[V];
+#pragma unroll
+        for (int w = 0; w < V; w++) allowed[w] = 0;
+        for (uint32_t k = 0; k < rl.x; k++) {
+            const uint4 pt = __ldg(&N.parts[rl.y + k]);
+#pragma unroll
+            for (int w = 0; w < V; w++)
+                if ((uint32_t)w == pt.y) allowed[w] |= pt.w << pt.z;
+        }
 #pragma unroll
         for (int w = 0; w < V; w++)
-            if ((uint32_t)w == pt.y) allowed[w] |= pt.w << pt.z;
+            if ((s[w] ^ t[w]) & ~allowed[w]) return false;
     }
-#pragma unroll
-    for (int w = 0; w < V; w++)
-        if ((s[w] ^ t[w]) & ~allowed[w]) return false;
     for (uint32_t k = 0; k < rl.x; k++) {
         const uint4 pt = __ldg(&N.parts[rl.y + k]);
         const uint32_t sq = field_get<V>(s, pt.y, pt.z, pt.w);

@@ -803,6 +803,20 @@ int gx_net_create(const gx_network_csr* c, void* stream, gx_net** out) {
             q[e + 3] = toff | (std::min<uint32_t>(nt, 255u) << 24);
         }
     }
+    // per rule, the bits its participants occupy in each of the first 4
+    // words (vlen <= 4): rule_generates rejects most dedup candidates with
+    // one 16-byte load instead of walking the participant list
+    const uint64_t rm_off = blob.size() + ((4 - blob.size() % 4) % 4);
+    blob.resize(rm_off + 4ull * std::max<uint32_t>(c->nrules, 1), 0u);
+    if (c->vlen <= 4) {
+        for (uint32_t r = 0; r < c->nrules; r++) {
+            const uint32_t np_ = c->rules[4 * r], po = c->rules[4 * r + 1];
+            for (uint32_t k = 0; k < np_; k++) {
+                const uint32_t* pt = c->parts + 4ull * (po + k);
+                if (pt[1] < 4) blob[rm_off + 4ull * r + pt[1]] |= pt[3] << pt[2];
+            }
+        }
+    }
     cudaError_t e = cudaMalloc(&n->d_blob, sizeof(uint32_t) * blob.size());
     if (e == cudaSuccess) e = cudaMalloc(&n->d_initial, sizeof(uint32_t) * 16);
     if (e != cudaSuccess) {
@@ -825,6 +839,7 @@ int gx_net_create(const gx_network_csr* c, void* stream, gx_net** out) {
     d.rq = (const uint2*)(n->d_blob + off[6]);
     d.rdst = n->d_blob + off[7];
     d.dedup = n->d_blob + off[8];
+    d.rmask = c->vlen <= 4 ? (const uint4*)(n->d_blob + rm_off) : nullptr;
     d.nproc = c->nproc;
     d.nrules = c->nrules;
     d.vlen = c->vlen;

@@ -47,6 +47,7 @@ struct NetDesc {
     const uint2* rq;        // {off, n}
     const uint32_t* rdst;
     const uint32_t* dedup;  // [n, rule...]
+    const uint4* rmask;     // per rule: participant bits of words 0..3 (vlen <= 4), or null
     uint32_t nproc, nrules, vlen, trig_packed;
     // the first GX_PROC_INLINE process descriptors again, in the parameter
     // (constant) bank: the expansion loop walks them in lockstep across the

@@ -210,31 +210,26 @@ def is_deadlock(net: Network, s: CompositeState) -> bool:
 
 # --------------------------------------------------------- device CSR
 
-def _rule_label_selfloops(net: Network, r: int) -> dict:
-    """process -> True if its column label of rule r has a self-loop anywhere."""
-    rule = net.rules[r]
-    out = {}
-    for i, lid in enumerate(rule.participants):
-        if lid is None:
-            continue
-        out[i] = any(tl == lid and s == d for s, tl, d in net.processes[i].transitions)
-    return out
-
-
 def _may_collide(net: Network, r1: int, r2: int) -> bool:
     """Can rules r1 and r2 (same result) ever fire to the same target from
-    the same source?  Only if every process in the symmetric difference of
-    their participant sets can stay put under its rule label (self-loop)."""
-    p1 = {i for i, l in enumerate(net.rules[r1].participants) if l is not None}
-    p2 = {i for i, l in enumerate(net.rules[r2].participants) if l is not None}
-    loops1 = _rule_label_selfloops(net, r1)
-    loops2 = _rule_label_selfloops(net, r2)
-    for i in p1 - p2:
-        if not loops1[i]:
-            return False
-    for i in p2 - p1:
-        if not loops2[i]:
-            return False
+    the same source (network.py expand() dedups (result, target) pairs)?
+    A common target t from source s needs, process by process:
+      * in both rules: some local state q where both rules' destination
+        lists intersect (t_i is in both);
+      * in one rule only: a local state q that is among that rule's own
+        destinations from q (the other rule leaves i at t_i = s_i = q).
+    The conditions are independent per process, so if any one of them is
+    unsatisfiable the pair never collides (a sound, state-blind test)."""
+    m1 = dict(net.rule_moves[r1])
+    m2 = dict(net.rule_moves[r2])
+    for i in set(m1) | set(m2):
+        if i in m1 and i in m2:
+            if not any(set(a) & set(b) for a, b in zip(m1[i], m2[i])):
+                return False
+        else:
+            per = m1[i] if i in m1 else m2[i]
+            if not any(q in dsts for q, dsts in enumerate(per)):
+                return False
     return True
 
 
