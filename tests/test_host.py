@@ -209,3 +209,38 @@ def test_cli_gen_model_and_input_errors(tmp_path, capsys):
     assert main(["explore", "--bucket-size", "5", "x"]) == 1
     assert main(["nonsense"]) == 1
 
+
+
+def test_may_collide_is_sound_on_reachable_states():
+    """network._may_collide prunes the device's same-result dedup checks; a
+    pair it calls collision-free must never produce a common (result,
+    target) from a reachable state.  Checked by brute force on every
+    reachable state of the small golden models (expand KATs)."""
+    from itertools import combinations, product
+    from paper_1801_05857_b200.network import _may_collide
+    kats = json.loads((GOLDEN / "expand_kats.json").read_text())
+    warnings.simplefilter("ignore")
+    checked = 0
+    for name in ("collide", "fig1", "gas3", "phil3", "rand3", "rand7"):
+        if name not in kats:
+            continue
+        net = load_network(model_path(name))
+        live = [r for r, m in enumerate(net.rule_moves) if m is not None]
+        pairs = [(a, b) for a, b in combinations(live, 2)
+                 if net.rules[a].result == net.rules[b].result and not _may_collide(net, a, b)]
+
+        def targets(r, s):
+            cols = net.rule_moves[r]
+            out = set()
+            for combo in product(*[per[s[i]] for i, per in cols]):
+                t = list(s)
+                for (i, _), d in zip(cols, combo):
+                    t[i] = d
+                out.add(tuple(t))
+            return out
+
+        for s, _, _ in kats[name]:
+            for a, b in pairs:
+                assert not (targets(a, s) & targets(b, s)), (name, a, b, s)
+                checked += 1
+    assert checked > 0
