@@ -43,7 +43,7 @@ sys.path.insert(0, str(ROOT))
 
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 TLB_REACH = 60 << 30    # one table beyond this: shard it on the GPU (profiles/README.md)
-SHARD_BYTES = 40 << 30  # target table bytes per shard
+SHARD_BYTES = 56 << 30  # table bytes per shard at most (ring19: 3 x 52 GB beat 4 x 39 GB)
 TRAFFIC = ROOT / "profiles" / "traffic.json"
 METRIC = "states explored/sec"
 
@@ -65,7 +65,7 @@ def parse():
                     help="one table, or hash-owner shards on this GPU (auto: shards once one "
                          "table would outgrow the TLB reach)")
     ap.add_argument("--shards", type=int, default=0, help="shard count (0 = auto)")
-    ap.add_argument("--inbox-frac", type=float, default=0.18,
+    ap.add_argument("--inbox-frac", type=float, default=0.2,
                     help="sharded engine: inbox keys per shard = frac * states / shards")
     ap.add_argument("--frontier-frac", type=float, default=0.035,
                     help="frontier vectors per shard = frac * states / shards")
@@ -417,6 +417,10 @@ def main():
         from paper_1801_05857_b200.distributed import LocalShardExplorer
         front = int(states_est * args.frontier_frac / shards) + (1 << 20)
         inbox = int(states_est * args.inbox_frac / shards) + (1 << 20)
+        # never more than what the tables and frontiers leave free
+        left = torch.cuda.mem_get_info()[0] - cap * 4 * shards - status_bytes * status \
+            - front * 4 * vlen * shards
+        inbox = max(1 << 20, min(inbox, int(0.85 * left) // (4 * vlen * shards)))
         ex = LocalShardExplorer(net, cfg, shards, inbox_capacity=inbox, frontier_capacity=front,
                                 status=status, stream=stream)
         total_slots = sum(sh.table.total_slots for sh in ex.shards)
