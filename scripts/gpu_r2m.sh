@@ -1,0 +1,8 @@
+# final round evidence: GPU tests, smoke, full default bench, reference arm, launch list
+set -x
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 600 2>&1 | tail -4 > gpurun_out/r2m_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2m_smoke.log 2>&1
+timeout 1800 python bench.py > gpurun_out/r2m_bench.json 2> gpurun_out/r2m_bench.err
+timeout 600 python bench.py --impl reference > gpurun_out/r2m_ref.json 2> gpurun_out/r2m_ref.err
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2m_launches.csv python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline --no-hash-bench --no-extra > /dev/null 2>&1
