@@ -80,14 +80,35 @@ __device__ __forceinline__ uint64_t bucket_of(const TableDesc& T, uint64_t h, in
     return fastmod(T.a[i] * h + T.b[i], T.nb, T.nb_magic);
 }
 
-// Owner rank of a key for hash-owner sharding: decorrelated from every
-// bucket index by a fresh splitmix finaliser of the fold value.
-__device__ __forceinline__ int owner_of(uint64_t h, int ranks) {
-    uint64_t z = h ^ 0x6A09E667F3BCC909ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    z ^= z >> 31;
-    return (int)(((z >> 32) * (uint64_t)ranks) >> 32);
+// A cheap 32-bit mix of a key (murmur3-style finaliser over its words): the
+// owner rank of hash-owner sharding and the dedup caches' slot index.  Not
+// the table hash (fold), so owners are decorrelated from bucket indices,
+// and four times cheaper than fold + a 64-bit finaliser.
+template <int V>
+__device__ __forceinline__ uint32_t key_mix(const uint32_t* key) {
+    uint32_t x = 0x9E3779B9u;
+#pragma unroll
+    for (int w = 0; w < V; w++) {
+        x = (x ^ key[w]) * 0x85EBCA77u;
+        x ^= x >> 13;
+    }
+    x *= 0xC2B2AE35u;
+    return x ^ (x >> 16);
+}
+
+__device__ __forceinline__ uint32_t key_mix_rt(const uint32_t* key, int v) {
+    uint32_t x = 0x9E3779B9u;
+    for (int w = 0; w < v; w++) {
+        x = (x ^ key[w]) * 0x85EBCA77u;
+        x ^= x >> 13;
+    }
+    x *= 0xC2B2AE35u;
+    return x ^ (x >> 16);
+}
+
+// owner rank in [0, ranks) of a key whose mix is x
+__device__ __forceinline__ int owner_of_mix(uint32_t x, int ranks) {
+    return (int)(((uint64_t)x * (uint64_t)ranks) >> 32);
 }
 
 __device__ __forceinline__ uint4 ldcg4(const uint32_t* p) {

@@ -305,7 +305,7 @@ __global__ void k_owner_hist(uint64_t salt, const uint32_t* __restrict__ keys, u
                              int ranks, unsigned long long* counts) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int o = owner_of(fold_rt(salt, keys + i * v, v), ranks);
+    const int o = owner_of_mix(key_mix_rt(keys + i * v, v), ranks);
     atomicAdd(&counts[o], 1ull);
 }
 
@@ -314,7 +314,7 @@ __global__ void k_owner_scatter(uint64_t salt, const uint32_t* __restrict__ keys
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t* k = keys + i * v;
-    const int o = owner_of(fold_rt(salt, k, v), ranks);
+    const int o = owner_of_mix(key_mix_rt(k, v), ranks);
     const unsigned long long p = atomicAdd(&cursor[o], 1ull);
     for (int w = 0; w < v; w++) out[p * v + w] = k[w];
 }
@@ -323,7 +323,7 @@ __global__ void k_owner_of(uint64_t salt, const uint32_t* __restrict__ keys, uin
                            int ranks, int32_t* out) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    out[i] = owner_of(fold_rt(salt, keys + i * v, v), ranks);
+    out[i] = owner_of_mix(key_mix_rt(keys + i * v, v), ranks);
 }
 
 // expand a frontier into a flat successor buffer (warp-aggregated append)

@@ -138,9 +138,8 @@ __device__ __forceinline__ uint32_t cache_filter(const TableDesc& T, unsigned lo
         for (int w = 0; w < V; w++) key[w] = a ? q[e * V + w] : 0u;
         bool keep = false;
         if (a) {
-            const uint64_t h = fold<V>(T.salt, key);
             const unsigned long long kv = cache_word<V>(T, key);
-            keep = atomicExch(&cache[(uint32_t)(h ^ (h >> 32)) & cmask], kv) != kv;
+            keep = atomicExch(&cache[key_mix<V>(key) & cmask], kv) != kv;
         }
         const uint32_t km = __ballot_sync(FULLMASK, keep);
         __syncwarp();
@@ -175,9 +174,8 @@ __device__ __forceinline__ uint32_t global_filter(const TableDesc& T, unsigned l
         for (int w = 0; w < V; w++) key[w] = a ? q[e * V + w] : 0u;
         bool keep = false;
         if (a) {
-            const uint64_t h = fold<V>(T.salt, key);
             const unsigned long long kv = cache_word<V>(T, key);
-            const uint32_t idx = (uint32_t)((h * 0xD6E8FEB86659FD93ull) >> 32) & gmask;
+            const uint32_t idx = (key_mix<V>(key) * 0x2545F491u) & gmask;
             keep = atomicExch(&gf[idx], kv) != kv;
         }
         const uint32_t km = __ballot_sync(FULLMASK, keep);
@@ -195,7 +193,7 @@ __device__ __forceinline__ uint32_t global_filter(const TableDesc& T, unsigned l
 
 // ------------------------------------------------ hash-owner routing
 // Multi-GPU: rank `rank` of `world` owns the keys whose
-// owner_of(fold) is `rank`.  The level kernel routes every successor it
+// owner_of_mix(key_mix(key)) is `rank`.  The level kernel routes every successor it
 // does not own straight into the owner's inbox over NVLink (peer pointers
 // from CUDA IPC; in one process, plain device pointers), reserving room
 // with one atomicAdd on the owner's inbox counter per (warp, owner,
@@ -246,7 +244,7 @@ __device__ __forceinline__ uint32_t route_remote(const TableDesc& T, const Route
             uint32_t key[V];
 #pragma unroll
             for (int w = 0; w < V; w++) key[w] = q[e * V + w];
-            o = owner_of(fold<V>(T.salt, key), world);
+            o = owner_of_mix(key_mix<V>(key), world);
         }
         const uint32_t grp = __match_any_sync(FULLMASK, o);
         if (o >= 0 && (grp & lanemask_lt()) == 0) cnt[o] += __popc(grp);
@@ -275,7 +273,7 @@ __device__ __forceinline__ uint32_t route_remote(const TableDesc& T, const Route
         if (e < m) {
 #pragma unroll
             for (int w = 0; w < V; w++) key[w] = q[e * V + w];
-            o = owner_of(fold<V>(T.salt, key), world);
+            o = owner_of_mix(key_mix<V>(key), world);
         }
         const uint32_t grp = __match_any_sync(FULLMASK, o);
         const uint32_t pos = (o >= 0 ? cur[o] : 0u) + __popc(grp & lanemask_lt());

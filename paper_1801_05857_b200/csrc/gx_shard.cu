@@ -1,7 +1,7 @@
 // gx_shard.cu -- hash-owner sharded exploration.
 //
 // One gx_shard per GPU (or, for tests on one GPU, several per device in
-// one process).  Shard r owns the states with owner_of(fold) == r and
+// one process).  Shard r owns the states with owner_of_mix(key_mix) == r and
 // holds that part of the state table.  One BFS level is two kernels with a
 // cross-GPU barrier between them:
 //

@@ -17,14 +17,20 @@ from conftest import ROOT, golden_models, model_path
 MASK = (1 << 64) - 1
 
 
-def owner_of(h: int, ranks: int) -> int:
-    """Python restatement of gx_device.cuh owner_of (pinned against the
-    device in test_gpu_distributed.py)."""
-    z = h ^ 0x6A09E667F3BCC909
-    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK
-    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK
-    z ^= z >> 31
-    return ((z >> 32) * ranks) >> 32
+def key_mix(words) -> int:
+    """Python restatement of gx_device.cuh key_mix (pinned against the
+    device in test_gpu_shards.py::test_owner_function_matches_restatement)."""
+    x = 0x9E3779B9
+    for w in words:
+        x = ((x ^ int(w)) * 0x85EBCA77) & 0xFFFFFFFF
+        x ^= x >> 13
+    x = (x * 0xC2B2AE35) & 0xFFFFFFFF
+    return x ^ (x >> 16)
+
+
+def owner_of(words, ranks: int) -> int:
+    """gx_device.cuh owner_of_mix(key_mix(key), ranks)."""
+    return (key_mix(words) * ranks) >> 32
 
 
 class OracleShard:
@@ -51,7 +57,7 @@ class OracleShard:
 
     def owner(self, packed):
         arr = np.asarray(packed, np.uint32).reshape(-1, self.vlen)
-        return np.array([owner_of(self.O.fold(self.salt, r), self.world) for r in arr])
+        return np.array([owner_of(r, self.world) for r in arr])
 
     def seed_frontier(self, packed):
         code, _ = self.table.find_or_insert(packed)

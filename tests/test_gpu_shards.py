@@ -123,3 +123,25 @@ def test_peterson6_single_table_equals_shards(tmp_path):
     assert (one.states, one.transitions, one.iterations, one.deadlocks_total) == \
         (three.states, three.transitions, three.iterations, three.deadlocks_total)
     assert one.states > 10 ** 8
+
+
+def test_owner_function_matches_restatement():
+    """gx_owner_of (the device's owner_of_mix(key_mix(key))) equals the
+    Python restatement the gloo driver tests use, for 1-4 word keys and
+    1..16 ranks."""
+    import numpy as np
+    from test_distributed import owner_of
+    from paper_1801_05857_b200.hashtable import StateTable
+    rng = np.random.default_rng(3)
+    for v in (1, 2, 3, 4):
+        t = StateTable(TableConfig(capacity_words=1 << 12), v)
+        try:
+            keys = rng.integers(0, 1 << 32, size=(500, v), dtype=np.uint64).astype(np.uint32)
+            for ranks in (1, 2, 3, 8, 16):
+                import ctypes as C
+                from paper_1801_05857_b200._lib import check, lib, ptr
+                out = np.zeros(len(keys), np.int32)
+                check(lib().gx_owner_of(t.handle, ptr(keys), len(keys), ranks, ptr(out, C.c_int32)))
+                assert out.tolist() == [owner_of(k, ranks) for k in keys], (v, ranks)
+        finally:
+            t.close()
