@@ -931,7 +931,7 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
         return GX_EINPUT;
     }
     // block-local dedup cache: cache_slots rounded down to a power of two,
-    // at most GX_CACHE_MAX_SLOTS and what keeps two blocks per SM resident
+    // at most GX_CACHE_MAX_SLOTS and what keeps GX_STAGED_MINB blocks per SM resident
     // (only for in-band tables with vlen <= 2)
     uint32_t cslots = 0;
     if (cfg->cache_slots > 0 && T.mode == MODE_MARK && v <= 2) {
