@@ -43,7 +43,7 @@ sys.path.insert(0, str(ROOT))
 
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 TLB_REACH = 60 << 30    # one table beyond this: shard it on the GPU (profiles/README.md)
-SHARD_BYTES = 56 << 30  # table bytes per shard at most (ring19: 3 x 52 GB beat 4 x 39 GB)
+SHARD_BYTES = 80 << 30  # table bytes per shard at most (ring19 sweep: 2 x 79 GB > 3 x 52 GB > 4 x 39 GB)
 TRAFFIC = ROOT / "profiles" / "traffic.json"
 METRIC = "states explored/sec"
 
@@ -65,7 +65,7 @@ def parse():
                     help="one table, or hash-owner shards on this GPU (auto: shards once one "
                          "table would outgrow the TLB reach)")
     ap.add_argument("--shards", type=int, default=0, help="shard count (0 = auto)")
-    ap.add_argument("--inbox-frac", type=float, default=0.2,
+    ap.add_argument("--inbox-frac", type=float, default=0.3,
                     help="sharded engine: inbox keys per shard = frac * states / shards")
     ap.add_argument("--frontier-frac", type=float, default=0.035,
                     help="frontier vectors per shard = frac * states / shards")

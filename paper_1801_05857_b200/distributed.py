@@ -535,7 +535,7 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, cl
     # (profiles/README.md); global shard id = rank * local + l
     per_gpu = cf[0] // world
     gpu_bytes = table_capacity(per_gpu, vlen, args.bucket_words, args.load) * 4
-    local = args.shards or max(1, -(-gpu_bytes // (56 << 30)))
+    local = args.shards or max(1, -(-gpu_bytes // (80 << 30)))
     gworld = world * local
     per_shard = cf[0] // gworld + (cf[0] >> 8) // gworld + 4096
     cap_words = table_capacity(per_shard, vlen, args.bucket_words, args.load)
