@@ -516,7 +516,7 @@ def main():
             "status_array": status,
             "l2_policy": "table re-zeroed every step; table >> 126 MB L2",
             "parallelism": "single GPU" if shards == 1 else
-            f"single GPU, {shards} hash-owner shards (each table inside the TLB reach; "
+            f"single GPU, {shards} hash-owner shards (one per <= 80 GiB of table, probed one at a time; "
             "fused peer-routed levels)",
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
