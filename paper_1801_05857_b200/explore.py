@@ -59,6 +59,11 @@ class ExploreConfig:
     # per insert) instead of the status-byte protocol; the table then has
     # vlen-4 slots (8 per 32-word bucket instead of 10)
     pad_vlen3: bool = True
+    # > 1: hash-partition the state space into this many shards on this GPU
+    # (the multi-GPU engine with local inboxes); `table` then sizes EACH
+    # shard.  Keeps each probed table range inside the TLB reach when one
+    # table would be tens of GB.  Dumps need shards == 1.
+    shards: int = 1
 
     def __post_init__(self):
         if self.workers < 1:
@@ -67,6 +72,8 @@ class ExploreConfig:
             raise ValueError("cache_slots must be >= 1")
         if self.backend not in BACKENDS:
             raise ValueError(f"unknown backend {self.backend!r}")
+        if self.shards < 1:
+            raise ValueError("shards must be >= 1")
 
 
 @dataclass(frozen=True)
@@ -222,6 +229,11 @@ class Explorer:
 def explore(net: Network, cfg: ExploreConfig, dump_states=None, dump_table=None):
     """Run the device reachability analysis and return its report
     (explore.py:300-395); optional canonical state dump and table CSV."""
+    if cfg.shards > 1:
+        if dump_states is not None or dump_table is not None:
+            raise ValueError("dump_states / dump_table need ExploreConfig(shards=1)")
+        from .distributed import explore_local_shards
+        return explore_local_shards(net, cfg, cfg.shards)
     ex = Explorer(net, cfg)
     try:
         report = ex.run()
