@@ -270,27 +270,32 @@ def hash_sweep(ra: dict):
 
 def duplication_sweep(ra: dict):
     """The paper's Fig. 4 protocol (bench.py:90-114,120-202): 2^28 FINDORPUT
-    ops over total/d unique random 1-word vectors, globally shuffled, table
-    sized for <= 50% load at d = 1; bucket 4 ("Gh-cbs") vs 32 ("Gh")."""
+    ops over total/d unique random vectors, globally shuffled, table sized
+    for <= 50% load at d = 1; bucket 4 ("Gh-cbs") vs 32 ("Gh"), 1-word
+    vectors (the paper's) and 2-word ones.  A cell whose
+    sizing overfills the buckets reports table_full (vlen 2 at bw 4: 2
+    slots per bucket at 50% load, as in the reference)."""
     from paper_1801_05857_b200.bench import (DuplicationSpec, device_insert_bench,
                                              insert_bench_table_config)
     from paper_1801_05857_b200.hashtable import StateTable
     total = 1 << 28
     out = []
-    for bw in (4, 8, 16, 32):
-        for d in (1, 10, 50, 100):
-            spec = DuplicationSpec(total=total, duplication=d, vector_length=1)
-            t = StateTable(insert_bench_table_config(spec, bw), 1, mark=(0, 31))
-            try:
-                r = device_insert_bench(t, total, d, seed=11)
-            finally:
-                t.close()
-            u = total // d
-            alg = (total * (4 + s_bw(bw)) + u * 32) / (r["ms"] / 1e3) / 1e9
-            r_g = ra.get(s_bw(bw), {}).get("gbs")
-            out.append({"bw": bw, "d": d, "ops_per_sec": r["ops_per_sec"], "inserted": r["inserted"],
-                        "found": r["found"], "gbs_alg": alg,
-                        "frac_of_random_roofline": alg / r_g if r_g else None})
+    for vlen in (1, 2):
+        for bw in (4, 8, 16, 32):
+            for d in ((1, 10, 50, 100) if vlen == 1 else (1, 10, 100)):
+                spec = DuplicationSpec(total=total, duplication=d, vector_length=vlen)
+                t = StateTable(insert_bench_table_config(spec, bw), vlen, mark=(vlen - 1, 31))
+                try:
+                    r = device_insert_bench(t, total, d, seed=11)
+                finally:
+                    t.close()
+                u = total // d
+                alg = (total * (4 * vlen + s_bw(bw)) + u * 32) / (r["ms"] / 1e3) / 1e9
+                r_g = ra.get(s_bw(bw), {}).get("gbs")
+                out.append({"vlen": vlen, "bw": bw, "d": d, "ops_per_sec": r["ops_per_sec"],
+                            "inserted": r["inserted"], "found": r["found"], "gbs_alg": alg,
+                            "frac_of_random_roofline": alg / r_g if r_g else None,
+                            "table_full": bool(r["full"])})
     return out
 
 
