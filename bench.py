@@ -225,16 +225,16 @@ def s_bw(bw: int) -> int:
 
 
 def hash_sweep(ra: dict):
-    """Isolated FINDORPUT throughput vs bucket size and fill (configs[1]):
-    an 8 GiB table of 1-word vectors (>> L2) filled step by step with fresh
-    random keys; at each fill f the next 2% of inserts and a lookup pass
-    over the same keys are timed.  K = 8 (the reference default) and K = 32
+    """Isolated FINDORPUT throughput vs bucket size and fill (configs[1],
+    SURVEY §8(d) protocol 2): a 32 GiB table of 1-word vectors (>> L2)
+    filled step by step with fresh random keys; at each fill f the next
+    2^28 inserts and a lookup pass over the same keys are timed.  K = 8 (the reference default) and K = 32
     (fill >= 0.6 needs it).  Algorithmic bytes per op:
     4 (key) + S(bw) (bucket) + 32 if inserted; frac against R(S(bw))."""
     from paper_1801_05857_b200.bench import device_insert_bench
     from paper_1801_05857_b200.hashtable import StateTable, TableConfig
     out = []
-    words = 1 << 31
+    words = 1 << 33
     for bw in (4, 8, 16, 32):
         r_g = ra.get(s_bw(bw), {}).get("gbs")
         for k in (8, 32):
@@ -244,7 +244,7 @@ def hash_sweep(ra: dict):
             done = 0
             for fill in (0.5, 0.6, 0.7, 0.8, 0.9):
                 target = int(fill * slots)
-                batch = int(0.02 * slots)
+                batch = min(1 << 28, int(0.02 * slots))
                 if target - batch > done:  # untimed fill to (fill - 2%)
                     r = device_insert_bench(t, target - batch - done, 1, seed=7, row_base=done)
                     done += r["inserted"]
@@ -269,8 +269,8 @@ def hash_sweep(ra: dict):
 
 
 def duplication_sweep(ra: dict):
-    """The paper's Fig. 4 protocol (bench.py:90-114,120-202): 2^28 FINDORPUT
-    ops over total/d unique random vectors, globally shuffled, table sized
+    """The paper's Fig. 4 protocol (bench.py:90-114,120-202): 2^30 FINDORPUT
+    ops (n >= 2^30) over total/d unique random vectors, globally shuffled, table sized
     for <= 50% load at d = 1; bucket 4 ("Gh-cbs") vs 32 ("Gh"), 1-word
     vectors (the paper's) and 2-word ones.  A cell whose
     sizing overfills the buckets reports table_full (vlen 2 at bw 4: 2
@@ -278,7 +278,7 @@ def duplication_sweep(ra: dict):
     from paper_1801_05857_b200.bench import (DuplicationSpec, device_insert_bench,
                                              insert_bench_table_config)
     from paper_1801_05857_b200.hashtable import StateTable
-    total = 1 << 28
+    total = 1 << 30
     out = []
     for vlen in (1, 2):
         for bw in (4, 8, 16, 32):
