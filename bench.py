@@ -226,9 +226,11 @@ def s_bw(bw: int) -> int:
 
 def hash_sweep(ra: dict):
     """Isolated FINDORPUT throughput vs bucket size and fill (configs[1],
-    SURVEY §8(d) protocol 2): a 32 GiB table of 1-word vectors (>> L2)
-    filled step by step with fresh random keys; at each fill f the next
-    2^28 inserts and a lookup pass over the same keys are timed.  K = 8 (the reference default) and K = 32
+    SURVEY §8(d) protocol 2): a 32 GiB table of 2-word vectors (>> L2;
+    1-word keys have only 2^31 distinct values next to the mark bit, too
+    few to fill it) filled step by step with fresh random keys; at each
+    fill f the next 2^28 inserts and a lookup pass over the same keys are
+    timed.  K = 8 (the reference default) and K = 32
     (fill >= 0.6 needs it).  Algorithmic bytes per op:
     4 (key) + S(bw) (bucket) + 32 if inserted; frac against R(S(bw))."""
     from paper_1801_05857_b200.bench import device_insert_bench
@@ -239,7 +241,7 @@ def hash_sweep(ra: dict):
         r_g = ra.get(s_bw(bw), {}).get("gbs")
         for k in (8, 32):
             t = StateTable(TableConfig(bucket_words=bw, num_hash_functions=k, capacity_words=words),
-                           1, mark=(0, 31))
+                           2, mark=(1, 31))
             slots = t.total_slots
             done = 0
             for fill in (0.5, 0.6, 0.7, 0.8, 0.9):
@@ -254,9 +256,9 @@ def hash_sweep(ra: dict):
                 r = device_insert_bench(t, batch, 1, seed=7, row_base=done)
                 done += r["inserted"]
                 look = device_insert_bench(t, batch, 1, seed=7, row_base=done - batch)
-                ins_gbs = r["ops_per_sec"] * (4 + s_bw(bw) + 32) / 1e9
-                look_gbs = look["ops_per_sec"] * (4 + s_bw(bw)) / 1e9
-                out.append({"bw": bw, "k": k, "fill": fill,
+                ins_gbs = r["ops_per_sec"] * (8 + s_bw(bw) + 32) / 1e9
+                look_gbs = look["ops_per_sec"] * (8 + s_bw(bw)) / 1e9
+                out.append({"vlen": 2, "bw": bw, "k": k, "fill": fill,
                             "insert_ops_per_sec": r["ops_per_sec"],
                             "lookup_ops_per_sec": look["ops_per_sec"],
                             "insert_gbs_alg": ins_gbs, "lookup_gbs_alg": look_gbs,
