@@ -136,6 +136,17 @@ int gx_read_slots(gx_table *t, const int64_t *handles, uint64_t n, uint8_t *stat
 int gx_dump(gx_table *t, int64_t *handles, uint8_t *status, uint32_t *words, uint64_t capacity,
             uint64_t *count);
 
+/* Order-independent multiset digest of the occupied slots: the set-level
+ * counterpart of the reference's sorted state dump (statevec.py:93-100,
+ * explore.py:376-383), for state spaces too large to dump.  Per occupied
+ * slot, over its first `words` words w_0..w_{n-1} (the packing scheme's
+ * vector length; a padding word is left out):
+ *     h = 0x6A09E667F3BCC908 ^ n;  h = mix64(h ^ w_i) for each i
+ * with mix64 the splitmix64 finaliser (hashtable.py:114-120 without the
+ * increment).  out[0] = count, out[1] = sum of h mod 2^64, out[2] = xor of
+ * h.  Shards combine by adding counts and sums and xor-ing xors. */
+int gx_table_digest(gx_table *t, int32_t words, uint64_t *out);
+
 /* --------------------------------------------------------------- network */
 
 /* A Network (network.py:43-62) flattened to device CSR by the host
@@ -174,7 +185,7 @@ typedef struct gx_explore_cfg {
     int32_t detect_deadlocks;
     int32_t filter_log2;        /* > 0: GPU-wide L2-resident dedup filter of 2^filter_log2
                                    entries (8 B each) in front of the table; 0 = off */
-    int64_t max_iterations;     /* <= 0: none */
+    int64_t max_iterations;     /* < 0: none; else stop once rounds >= it (explore.py:256-261) */
     uint64_t frontier_capacity; /* vectors; 0 = size from free device memory */
     int32_t probe_group;        /* 0 = auto; else lanes per bucket probe (1,2,4,8) */
     int32_t cache_slots;        /* per-block shared-memory dedup cache entries (the
@@ -274,6 +285,24 @@ int gx_shard_absorb(gx_shard *s, uint64_t *stats);
  * after the last chunk gx_shard_end_level returns the level's stats.
  * gx_shard_frontier gives the current frontier size. */
 int gx_shard_expand_range(gx_shard *s, uint64_t begin, uint64_t count);
+
+/* Partitioned dedup mode (gx_part.cuh).  dedup != 0: the
+ * expansion routes EVERY successor (own ones too) into the owner shard's
+ * inbox, split into `nsub` hash sub-partitions; the absorb step filters each
+ * sub-partition through a 2^set_log2 x 32-byte L2-resident set so that only
+ * the first occurrence of a key in the chunk probes the table.  Results are
+ * those of the fused mode (FINDORPUT is idempotent, hashtable.py:224-280).
+ * gx_shard_set_partitions sets nsub for the next chunk (same on every
+ * shard; world * nsub <= 128); gx_shard_chunk_status (after the expansion,
+ * synchronising) gives out[0] = this shard's inbox-overflow flag, out[1] =
+ * successors routed so far this run, out[2] = states expanded so far; when
+ * any shard overflowed, every shard calls gx_shard_rollback (the chunk's
+ * counters and routed keys are discarded) and the driver re-expands the
+ * chunk in smaller pieces. */
+int gx_shard_set_mode(gx_shard *s, int32_t dedup, int32_t set_log2);
+int gx_shard_set_partitions(gx_shard *s, uint32_t nsub);
+int gx_shard_chunk_status(gx_shard *s, uint64_t *out);
+int gx_shard_rollback(gx_shard *s);
 int gx_shard_absorb_chunk(gx_shard *s);
 int gx_shard_end_level(gx_shard *s, uint64_t *stats);
 int gx_shard_frontier(const gx_shard *s, uint64_t *n);

@@ -97,6 +97,10 @@ def lib():
         L.or_probe_raw.argtypes = [C.c_uint64, C.c_int, C.c_uint64, u32p, C.c_int, u64p]
         L.or_py_tuple_hash.restype = C.c_int64
         L.or_py_tuple_hash.argtypes = [u32p, C.c_int]
+        L.or_state_hash.restype = C.c_uint64
+        L.or_state_hash.argtypes = [u32p, C.c_int]
+        L.or_table_digest.argtypes = [C.c_void_p, C.c_int, u64p]
+        L.or_ring_digest.argtypes = [C.c_int, C.c_int, u64p]
         _lib = L
     return _lib
 
@@ -143,6 +147,20 @@ def slots_per_bucket(bw: int, vlen: int, layout: int) -> int:
 def py_tuple_hash(p) -> int:
     arr = np.asarray(p, np.uint32)
     return int(lib().or_py_tuple_hash(_ptr(arr, C.c_uint32), len(arr)))
+
+
+def state_hash(p) -> int:
+    arr = np.ascontiguousarray(p, np.uint32)
+    return int(lib().or_state_hash(_ptr(arr, C.c_uint32), len(arr)))
+
+
+def ring_digest(n: int, threads: int = 0) -> tuple:
+    """(count, sum, xor) digest of token ring N's reachable set, enumerated
+    in closed form (gx_oracle.c or_ring_digest)."""
+    out = np.zeros(3, np.uint64)
+    if lib().or_ring_digest(n, threads or os.cpu_count() or 1, _ptr(out, C.c_uint64)):
+        raise ValueError(_err())
+    return int(out[0]), int(out[1]), int(out[2])
 
 
 # -------------------------------------------------------------------- table
@@ -217,6 +235,12 @@ class Table:
         out = np.zeros(self.vlen, np.uint32)
         lib().or_read_slot(self._h, h, _ptr(out, C.c_uint32))
         return tuple(int(x) for x in out)
+
+    def digest(self, words: int | None = None) -> tuple:
+        """(count, sum, xor) set digest of the occupied slots (gx_table_digest)."""
+        out = np.zeros(3, np.uint64)
+        lib().or_table_digest(self._h, int(words or self.vlen), _ptr(out, C.c_uint64))
+        return int(out[0]), int(out[1]), int(out[2])
 
     def occupied(self):
         """(handles, statuses, words[n, vlen]) in bucket-major order."""

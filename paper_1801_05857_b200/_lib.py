@@ -76,6 +76,7 @@ SIGNATURES = {
     "gx_occupancy": (C.c_int, [_vp, _u64p, _u64p]),
     "gx_read_slots": (C.c_int, [_vp, _i64p, C.c_uint64, _u8p, _u32p]),
     "gx_dump": (C.c_int, [_vp, _i64p, _u8p, _u32p, C.c_uint64, _u64p]),
+    "gx_table_digest": (C.c_int, [_vp, C.c_int32, _u64p]),
     "gx_net_create": (C.c_int, [_P(NetworkCsr), _vp, _P(_vp)]),
     "gx_net_destroy": (C.c_int, [_vp]),
     "gx_expand": (C.c_int, [_vp, _u32p, C.c_uint64, _u64p, _u32p, _u32p, C.c_uint64, _u64p]),
@@ -104,6 +105,10 @@ SIGNATURES = {
     "gx_shard_absorb": (C.c_int, [_vp, _u64p]),
     "gx_shard_expand_range": (C.c_int, [_vp, C.c_uint64, C.c_uint64]),
     "gx_shard_absorb_chunk": (C.c_int, [_vp]),
+    "gx_shard_set_mode": (C.c_int, [_vp, C.c_int32, C.c_int32]),
+    "gx_shard_set_partitions": (C.c_int, [_vp, C.c_uint32]),
+    "gx_shard_chunk_status": (C.c_int, [_vp, _u64p]),
+    "gx_shard_rollback": (C.c_int, [_vp]),
     "gx_shard_end_level": (C.c_int, [_vp, _u64p]),
     "gx_shard_frontier": (C.c_int, [_vp, _u64p]),
     "gx_shard_finish": (C.c_int, [_vp, _P(Report), _u32p]),

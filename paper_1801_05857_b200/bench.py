@@ -242,6 +242,33 @@ def gen_gas_station(customers: int, out_dir) -> tuple:
     return paths, _write_net(out, rules, files, f"gas station: one operator, two pumps, {n} customers")
 
 
+def gen_philosophers(n: int, out_dir) -> tuple:
+    """Dining philosophers, left fork first: the deadlocking family of
+    SURVEY §8(f2) (a generator in the reference's pattern, bench.py:245-359).
+    N philosophers (takeL, takeR, putL, putR) and N forks (take, put); rule
+    (i, a) synchronises philosopher i's action a with fork i (left) or fork
+    i+1 mod N (right).  Exactly one deadlock: every philosopher holding its
+    left fork.  2..16 philosophers (vlen 1 up to 10, 2 beyond)."""
+    if not 2 <= n <= 16:
+        raise ValueError("philosophers supports 2..16")
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    phil, fork = out / "phil.aut", out / "fork.aut"
+    phil.write_text('des (0, 4, 4)\n(0, "takeL", 1)\n(1, "takeR", 2)\n(2, "putL", 3)\n'
+                    '(3, "putR", 0)\n', encoding="utf-8")
+    fork.write_text('des (0, 2, 2)\n(0, "take", 1)\n(1, "put", 0)\n', encoding="utf-8")
+    total = 2 * n
+    rules = []
+    for i in range(n):
+        left, right = n + i, n + (i + 1) % n
+        for act, f, fact in (("takeL", left, "take"), ("takeR", right, "take"),
+                             ("putL", left, "put"), ("putR", right, "put")):
+            rules.append(_rule(total, [(i, act), (f, fact)], f"{act}{i}"))
+    files = ['"phil.aut"'] * n + ['"fork.aut"'] * n
+    return [phil, fork], _write_net(out, rules, files,
+                                    f"dining philosophers, {n} philosophers, left fork first")
+
+
 def gen_peterson(procs: int, out_dir) -> tuple:
     """Peterson's N-process filter lock as a network of LTSs (the BEEM
     "peterson" family the paper's peterson7 row comes from).

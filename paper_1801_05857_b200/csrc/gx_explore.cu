@@ -755,6 +755,60 @@ void keep_smallest(const gx_net* n, std::vector<uint32_t>& kept, const uint32_t*
 
 static int persistent_grid() { return sm_count() * 8; }
 
+// Deadlock states of frontier F[0, n) (count == 0), recorded in dl with the
+// counter cell (the fallback of a level that found more deadlocks than its
+// record buffer holds; explore.py:220-226 keeps the 100 smallest of ALL).
+template <int V>
+__global__ void k_dl_scan(NetDesc N, const uint32_t* __restrict__ F, uint64_t n, uint32_t* dl,
+                          unsigned long long* cell) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t s[V];
+    load_state<V>(F + i * V, s);
+    uint64_t c;
+    expand_state<V, false>(N, s, &c, 0, 0, nullptr);
+    if (c == 0) store_state<V>(dl + atomicAdd(cell, 1ull) * V, s);
+}
+
+typedef void (*dl_scan_t)(NetDesc, const uint32_t*, uint64_t, uint32_t*, unsigned long long*);
+
+static dl_scan_t pick_dl_scan(int v) {
+    switch (v) {
+#define GX_CASE(X) \
+    case X: return k_dl_scan<X>;
+        GX_CASE(1) GX_CASE(2) GX_CASE(3) GX_CASE(4) GX_CASE(5) GX_CASE(6) GX_CASE(7) GX_CASE(8)
+        GX_CASE(9) GX_CASE(10) GX_CASE(11) GX_CASE(12) GX_CASE(13) GX_CASE(14) GX_CASE(15)
+        GX_CASE(16)
+#undef GX_CASE
+    }
+    return nullptr;
+}
+
+// Re-expand the frontier F[0, nF) in chunks of dl_cap states (so no chunk
+// can overflow the record buffer dl) and merge every chunk's deadlocks into
+// `kept`: exact 100 smallest however many deadlocks one level has.
+int rescan_deadlocks(const gx_net* n, const uint32_t* F, uint64_t nF, uint32_t* dl, uint64_t dl_cap,
+                     unsigned long long* cell, cudaStream_t st, std::vector<uint32_t>& kept) {
+    const uint32_t v = n->vlen;
+    dl_scan_t k = pick_dl_scan((int)v);
+    std::vector<uint32_t> host;
+    for (uint64_t b = 0; b < nF; b += dl_cap) {
+        const uint64_t m = std::min<uint64_t>(dl_cap, nF - b);
+        GX_CUDA(cudaMemsetAsync(cell, 0, 8, st));
+        k<<<(int)((m + 255) / 256), 256, 0, st>>>(n->d, F + b * v, m, dl, cell);
+        GX_LAUNCHED();
+        unsigned long long c = 0;
+        GX_CUDA(cudaMemcpyAsync(&c, cell, 8, cudaMemcpyDeviceToHost, st));
+        GX_CUDA(cudaStreamSynchronize(st));
+        if (!c) continue;
+        host.resize(c * v);
+        GX_CUDA(cudaMemcpyAsync(host.data(), dl, sizeof(uint32_t) * c * v, cudaMemcpyDeviceToHost, st));
+        GX_CUDA(cudaStreamSynchronize(st));
+        keep_smallest(n, kept, host.data(), c);
+    }
+    return GX_OK;
+}
+
 }  // namespace gx
 
 using namespace gx;
@@ -1052,12 +1106,17 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
             nnew = hc[LV_NEW] - new_base;
             new_base = hc[LV_NEW];
             if (hc[LV_DL] > dl_base) {
-                const uint64_t d = std::min<uint64_t>(hc[LV_DL] - dl_base, dl_cap);
-                dlhost.resize(d * v);
-                GX_CUDA(cudaMemcpyAsync(dlhost.data(), n->dl.p, sizeof(uint32_t) * d * v,
-                                        cudaMemcpyDeviceToHost, st));
-                GX_CUDA(cudaStreamSynchronize(st));
-                keep_smallest(n, kept, dlhost.data(), d);
+                const uint64_t d = hc[LV_DL] - dl_base;
+                if (d <= dl_cap) {
+                    dlhost.resize(d * v);
+                    GX_CUDA(cudaMemcpyAsync(dlhost.data(), n->dl.p, sizeof(uint32_t) * d * v,
+                                            cudaMemcpyDeviceToHost, st));
+                    GX_CUDA(cudaStreamSynchronize(st));
+                    keep_smallest(n, kept, dlhost.data(), d);
+                } else {  // the buffer overflowed: re-derive this level's deadlocks in chunks
+                    rc = rescan_deadlocks(n, F, nF, (uint32_t*)n->dl.p, dl_cap, ctr + CTR_SCRATCH, st, kept);
+                    if (rc) return rc;
+                }
                 dl_base = hc[LV_DL];
             }
             if (hc[LV_OVF]) {
@@ -1077,7 +1136,7 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
                 break;
             }
             if (claims == 0) break;
-            if (cfg->max_iterations > 0 && rounds >= (uint64_t)cfg->max_iterations) {
+            if (cfg->max_iterations >= 0 && rounds >= (uint64_t)cfg->max_iterations) {
                 outcome = GX_ITERATION_CAP;
                 break;
             }
@@ -1182,6 +1241,15 @@ int gx_expand_route(gx_net* n, const gx_table* t, const uint32_t* d_front, uint6
     if (transitions) *transitions = h[1];
     if (deadlocks) *deadlocks = h[2];
     n->dl_recorded = std::min<uint64_t>(h[2], dl_cap);
+    if (h[2] > dl_cap) {
+        // more deadlocks than records: the exact 100 smallest, left in dl
+        std::vector<uint32_t> kept;
+        rc = rescan_deadlocks(n, d_front, nfront, (uint32_t*)n->dl.p, dl_cap, c + 4, st, kept);
+        if (rc) return rc;
+        GX_CUDA(cudaMemcpyAsync(n->dl.p, kept.data(), sizeof(uint32_t) * kept.size(), cudaMemcpyHostToDevice, st));
+        GX_CUDA(cudaStreamSynchronize(st));
+        n->dl_recorded = kept.size() / v;
+    }
     return GX_OK;
 }
 

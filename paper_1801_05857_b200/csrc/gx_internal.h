@@ -117,4 +117,7 @@ int table_find_or_put_dev(gx_table* t, const uint32_t* d_keys, uint64_t n, uint8
 int table_fixup_status(gx_table* t, const uint32_t* d_new_keys, uint64_t n_new);
 // keep the GX_DEADLOCK_KEEP smallest deadlock states (composite order)
 void keep_smallest(const gx_net* n, std::vector<uint32_t>& kept, const uint32_t* add, uint64_t cnt);
+// the exact deadlocks of frontier F[0, nF) merged into kept, dl_cap states at a time
+int rescan_deadlocks(const gx_net* n, const uint32_t* F, uint64_t nF, uint32_t* dl, uint64_t dl_cap,
+                     unsigned long long* cell, cudaStream_t st, std::vector<uint32_t>& kept);
 }  // namespace gx

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "gx_level.cuh"
+#include "gx_part.cuh"
 
 namespace gx {
 
@@ -77,6 +78,127 @@ __global__ void __launch_bounds__(256, GX_STAGED_MINB) k_absorb(TableDesc T, Lev
     if (lane == 0 && probes) atomicAdd(&A.ctr[LV_PROBES], probes);
 }
 
+// ---- partitioned dedup mode (gx_part.cuh) ----------------------------
+// K1: expand + route every successor into its partition (no table access)
+template <int V>
+__global__ void __launch_bounds__(256, 2) k_level_part(TableDesc T, NetDesc N, LevelArgs A, RouteArgs R,
+                                                       PartArgs P) {
+    level_part_body<V>(T, N, A, R, P);
+}
+
+// K2: one sub-partition of this shard: drop keys already seen in this chunk
+// (L2 set), FINDORPUT the first occurrences, append the inserted to the
+// next frontier.  Keys arrive with the mark bit set.
+template <int BW, int V>
+__global__ void __launch_bounds__(256, GX_STAGED_MINB) k_absorb_dedup(TableDesc T, LevelArgs A,
+                                                                      const uint32_t* __restrict__ keys,
+                                                                      const unsigned long long* count,
+                                                                      uint64_t cap, void* set, uint32_t groups) {
+    using L = StagedSmem<BW, V>;
+    using S = Staged<BW, V>;
+    constexpr int QCAP = QWORDS / V;
+    constexpr int KPL = 4;  // keys per lane with their set lookups in flight
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * QWORDS;
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::KB;
+    uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
+    const uint64_t n = min((uint64_t)*count, cap);
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    unsigned long long probes = 0;
+    const uint32_t unmark = ~T.mark;
+    for (uint64_t base = warp * QCAP; base < n; base += nwarps * QCAP) {
+        const uint32_t m0 = (uint32_t)min((uint64_t)QCAP, n - base);
+        uint32_t kept = 0;
+        for (uint32_t r0 = 0; r0 < m0; r0 += 32 * KPL) {
+            uint32_t km[KPL][V];
+            bool first[KPL];
+#pragma unroll
+            for (int i = 0; i < KPL; i++) {
+                const uint32_t e = r0 + i * 32 + lane;
+                const bool a = e < m0;
+                if (a) {
+                    if (V == 2) {
+                        const uint2 x = __ldcs(reinterpret_cast<const uint2*>(keys + (base + e) * 2));
+                        km[i][0] = x.x;
+                        km[i][1 % V] = x.y;
+                    } else if (V == 4) {
+                        const uint4 x = __ldcs(reinterpret_cast<const uint4*>(keys + (base + e) * 4));
+                        km[i][0] = x.x;
+                        km[i][1 % V] = x.y;
+                        km[i][2 % V] = x.z;
+                        km[i][3 % V] = x.w;
+                    } else {
+#pragma unroll
+                        for (int w = 0; w < V; w++) km[i][w] = __ldcs(keys + (base + e) * V + w);
+                    }
+                } else {
+#pragma unroll
+                    for (int w = 0; w < V; w++) km[i][w] = 0u;
+                }
+                bool marked = false;  // a written slot carries the mark bit
+#pragma unroll
+                for (int w = 0; w < V; w++) marked |= (km[i][w] & (w == (int)T.mark_word ? T.mark : 0u)) != 0u;
+                first[i] = a && marked;
+            }
+#pragma unroll
+            for (int i = 0; i < KPL; i++)
+                if (first[i]) first[i] = dedup_first<V>(set, groups, km[i]);
+#pragma unroll
+            for (int i = 0; i < KPL; i++) {
+                const uint32_t msk = __ballot_sync(FULLMASK, first[i]);
+                if (first[i]) {
+                    const uint32_t p = kept + __popc(msk & lanemask_lt());
+#pragma unroll
+                    for (int w = 0; w < V; w++) q[p * V + w] = w == (int)T.mark_word ? (km[i][w] & unmark) : km[i][w];
+                }
+                kept += __popc(msk);
+            }
+        }
+        __syncwarp();
+        probes += lane == 0 ? kept : 0;
+        uint32_t full = 0;
+        const uint32_t n_out = probe_staged<BW, V>(T, q, kept, stage, sbkt, &full);
+        if (__any_sync(FULLMASK, full != 0u) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
+        if (n_out) flush_out<V>(A, q, n_out);
+        __syncwarp();
+    }
+    probes = warp_sum(probes);
+    if (lane == 0 && probes) atomicAdd(&A.ctr[LV_PROBES], probes);
+}
+
+typedef void (*part_kernel_t)(TableDesc, NetDesc, LevelArgs, RouteArgs, PartArgs);
+typedef void (*dedup_kernel_t)(TableDesc, LevelArgs, const uint32_t*, const unsigned long long*, uint64_t,
+                               void*, uint32_t);
+
+struct PartKernels {
+    part_kernel_t a;
+    dedup_kernel_t b;
+    size_t smem_a, smem_b;
+};
+
+template <int BW>
+static PartKernels pick_part_v(int v) {
+    switch (v) {
+        case 1: return {k_level_part<1>, k_absorb_dedup<BW, 1>, PartSmem<1>::FIXED, StagedSmem<BW, 1>::FIXED};
+        case 2: return {k_level_part<2>, k_absorb_dedup<BW, 2>, PartSmem<2>::FIXED, StagedSmem<BW, 2>::FIXED};
+        case 4: return {k_level_part<4>, k_absorb_dedup<BW, 4>, PartSmem<4>::FIXED, StagedSmem<BW, 4>::FIXED};
+    }
+    return {nullptr, nullptr, 0, 0};
+}
+
+static PartKernels pick_part(const TableDesc& T) {
+    switch (T.bw) {
+        case 4: return pick_part_v<4>((int)T.vlen);
+        case 8: return pick_part_v<8>((int)T.vlen);
+        case 16: return pick_part_v<16>((int)T.vlen);
+        case 32: return pick_part_v<32>((int)T.vlen);
+    }
+    return {nullptr, nullptr, 0, 0};
+}
+
 typedef void (*routed_kernel_t)(TableDesc, NetDesc, LevelArgs, RouteArgs);
 typedef void (*absorb_kernel_t)(TableDesc, LevelArgs, const uint32_t*, const unsigned long long*, uint64_t);
 
@@ -106,7 +228,9 @@ static ShardKernels pick_shard(const TableDesc& T) {
     return {nullptr, nullptr, 0};
 }
 
-static constexpr size_t INBOX_HEAD = 256;  // counter cell, padded
+// inbox head: the per-sub-partition cursors and the overflow cell
+// (gx_part.cuh PART_HEAD), padded so the keys start 4 KB aligned
+static constexpr size_t INBOX_HEAD = (PART_HEAD + 4095) & ~size_t(4095);
 
 }  // namespace gx
 
@@ -147,6 +271,15 @@ struct gx_shard {
     double level_ms = 0;
     int32_t detect = 0;
     bool level_open = false;  // LevelArgs of the current level are set
+    // partitioned dedup mode (gx_shard_set_mode)
+    bool dedup = false;
+    PartKernels P{};
+    uint32_t nsub = 1;
+    uint64_t cap_sub = 0;
+    DevBuf set;
+    uint32_t set_groups = 0;
+    DevBuf snap;  // level counters before the current chunk's expansion (rollback)
+    size_t smem_a = 0;
 };
 
 extern "C" {
@@ -228,6 +361,8 @@ int gx_shard_destroy(gx_shard* s) {
     s->fb.release();
     s->dl.release();
     s->gf.release();
+    s->set.release();
+    s->snap.release();
     for (cudaEvent_t e : s->ev) cudaEventDestroy(e);
     delete s;
     return GX_OK;
@@ -380,6 +515,50 @@ static void level_args(gx_shard* s) {
     s->level_open = true;
 }
 
+int gx_shard_set_mode(gx_shard* s, int32_t dedup, int32_t set_log2) {
+    if (!dedup) {
+        s->dedup = false;
+        return GX_OK;
+    }
+    const TableDesc& T = s->t->d;
+    PartKernels P = pick_part(T);
+    if (!P.a) {
+        set_error("no partitioned level kernels for bw=%u vlen=%u", T.bw, T.vlen);
+        return GX_EINPUT;
+    }
+    if (set_log2 < 10 || set_log2 > 26) {
+        set_error("dedup set of 2^%d groups outside 2^10..2^26", set_log2);
+        return GX_EINPUT;
+    }
+    s->P = P;
+    s->set_groups = 1u << set_log2;
+    int rc = s->set.ensure(32ull * s->set_groups);
+    if (!rc) rc = s->snap.ensure(sizeof(uint64_t) * CTR_N);
+    if (rc) return rc;
+    // the K1 queue cache (block-local, optional) rides after its fixed part
+    s->smem_a = ((P.smem_a + 15) & ~size_t(15)) + 8 * (size_t)s->cslots;
+    if (s->smem_a > STAGED_SMEM_BUDGET * GX_STAGED_MINB / 2) {  // keep 2 blocks per SM
+        s->smem_a = (P.smem_a + 15) & ~size_t(15);
+    }
+    GX_CUDA(cudaFuncSetAttribute((const void*)P.a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_a));
+    GX_CUDA(cudaFuncSetAttribute((const void*)P.b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_b));
+    s->dedup = true;
+    s->nsub = 1;
+    s->cap_sub = s->inbox_cap;
+    return GX_OK;
+}
+
+int gx_shard_set_partitions(gx_shard* s, uint32_t nsub) {
+    if (nsub < 1 || nsub > GX_PART_SUB_MAX || (uint64_t)nsub * s->world > GX_PART_BINS_MAX) {
+        set_error("%u sub-partitions x %d shards outside the routing limits (%d per shard, %d bins)", nsub,
+                  s->world, GX_PART_SUB_MAX, GX_PART_BINS_MAX);
+        return GX_EINPUT;
+    }
+    s->nsub = nsub;
+    s->cap_sub = s->inbox_cap / nsub;
+    return GX_OK;
+}
+
 int gx_shard_expand_range(gx_shard* s, uint64_t begin, uint64_t count) {
     gx_table* t = s->t;
     const uint32_t v = t->d.vlen;
@@ -390,6 +569,25 @@ int gx_shard_expand_range(gx_shard* s, uint64_t begin, uint64_t count) {
     A.front = s->F + begin * v;
     A.nfront = count;
     cudaEvent_t a0 = next_event(s), a1 = next_event(s);
+    if (s->dedup) {
+        // counters before this chunk: gx_shard_rollback restores them
+        GX_CUDA(cudaMemcpyAsync(s->snap.p, t->d_ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToDevice,
+                                s->stream));
+        GX_CUDA(cudaEventRecord(a0, s->stream));
+        if (count) {
+            PartArgs P;
+            P.nsub = s->nsub;
+            P.pad = 0;
+            P.cap_sub = s->cap_sub;
+            A.cache_mask = s->smem_a > ((s->P.smem_a + 15) & ~size_t(15)) && s->cslots ? s->cslots - 1 : 0;
+            const uint64_t want = (count + 31) / 32;
+            const int g = (int)std::min<uint64_t>((uint64_t)sm_count() * 2, (want + 7) / 8);
+            s->P.a<<<g, 256, s->smem_a, s->stream>>>(t->d, s->n->d, A, s->R, P);
+            GX_LAUNCHED();
+        }
+        GX_CUDA(cudaEventRecord(a1, s->stream));
+        return GX_OK;
+    }
     GX_CUDA(cudaEventRecord(a0, s->stream));
     if (count) {
         const uint64_t want = (count + 31) / 32;
@@ -408,10 +606,50 @@ int gx_shard_frontier(const gx_shard* s, uint64_t* n) {
     return GX_OK;
 }
 
+int gx_shard_chunk_status(gx_shard* s, uint64_t* out) {
+    uint64_t ovf = 0;
+    GX_CUDA(cudaMemcpyAsync(&ovf, (char*)s->inbox_block + 8 * GX_PART_SUB_MAX, 8, cudaMemcpyDeviceToHost,
+                            s->stream));
+    GX_CUDA(cudaMemcpyAsync(s->t->h_ctr, s->t->d_ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost,
+                            s->stream));
+    GX_CUDA(cudaStreamSynchronize(s->stream));
+    out[0] = ovf;
+    out[1] = s->t->h_ctr[LV_ROUTED];
+    out[2] = s->t->h_ctr[LV_EXP];
+    return GX_OK;
+}
+
+int gx_shard_rollback(gx_shard* s) {
+    if (!s->dedup) {
+        set_error("rollback needs the partitioned mode");
+        return GX_EINPUT;
+    }
+    GX_CUDA(cudaMemcpyAsync(s->t->d_ctr, s->snap.p, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToDevice,
+                            s->stream));
+    GX_CUDA(cudaMemsetAsync(s->inbox_block, 0, 8 * (GX_PART_SUB_MAX + 1), s->stream));
+    return GX_OK;
+}
+
 int gx_shard_absorb_chunk(gx_shard* s) {
     gx_table* t = s->t;
     cudaStream_t st = s->stream;
     if (!s->level_open) level_args(s);
+    if (s->dedup) {
+        unsigned long long* cur = (unsigned long long*)s->inbox_block;
+        const uint32_t* keys = (const uint32_t*)((char*)s->inbox_block + INBOX_HEAD);
+        cudaEvent_t b0 = next_event(s), b1 = next_event(s);
+        GX_CUDA(cudaEventRecord(b0, st));
+        for (uint32_t sub = 0; sub < s->nsub; sub++) {
+            GX_CUDA(cudaMemsetAsync(s->set.p, 0, 32ull * s->set_groups, st));
+            s->P.b<<<sm_count() * GX_STAGED_MINB, 256, s->P.smem_b, st>>>(
+                t->d, s->A, keys + (uint64_t)sub * s->cap_sub * t->d.vlen, cur + sub, s->cap_sub, s->set.p,
+                s->set_groups);
+            GX_LAUNCHED();
+        }
+        GX_CUDA(cudaEventRecord(b1, st));
+        GX_CUDA(cudaMemsetAsync(s->inbox_block, 0, 8 * (GX_PART_SUB_MAX + 1), st));
+        return GX_OK;
+    }
     // asynchronous: the inbox fill is only known on the device (a
     // persistent grid exits at once when nothing arrived, and flags an
     // overflowing inbox in LV_OVF); the counter is reset in stream order
@@ -444,11 +682,17 @@ int gx_shard_end_level(gx_shard* s, uint64_t* stats) {
     const uint64_t nnew = hc[LV_NEW] - s->new_base;
     s->new_base = hc[LV_NEW];
     if (hc[LV_DL] > s->dl_base) {
-        const uint64_t d = std::min<uint64_t>(hc[LV_DL] - s->dl_base, s->dl_cap);
-        s->dlhost.resize(d * v);
-        GX_CUDA(cudaMemcpyAsync(s->dlhost.data(), s->dl.p, sizeof(uint32_t) * d * v, cudaMemcpyDeviceToHost, st));
-        GX_CUDA(cudaStreamSynchronize(st));
-        keep_smallest(s->n, s->kept, s->dlhost.data(), d);
+        const uint64_t d = hc[LV_DL] - s->dl_base;
+        if (d <= s->dl_cap) {
+            s->dlhost.resize(d * v);
+            GX_CUDA(cudaMemcpyAsync(s->dlhost.data(), s->dl.p, sizeof(uint32_t) * d * v, cudaMemcpyDeviceToHost, st));
+            GX_CUDA(cudaStreamSynchronize(st));
+            keep_smallest(s->n, s->kept, s->dlhost.data(), d);
+        } else {  // overflowed record buffer: re-derive this level's deadlocks exactly
+            int rc = rescan_deadlocks(s->n, s->F, s->nF, (uint32_t*)s->dl.p, s->dl_cap,
+                                      (unsigned long long*)t->d_ctr + CTR_SCRATCH, st, s->kept);
+            if (rc) return rc;
+        }
         s->dl_base = hc[LV_DL];
     }
     s->states += nnew;

@@ -430,6 +430,79 @@ __global__ void k_mark_new(TableDesc T, const int64_t* __restrict__ handles, uin
     T.status[bucket * (uint64_t)T.stride + j] = T.mode == MODE_STATUS ? NEW : 0;
 }
 
+// ----------------------------------------------------------- set digest
+// Order-independent digest of the occupied slots (include/gx.h
+// gx_table_digest): per state the hash of its first `words` words (mark bit
+// cleared), summed mod 2^64 and xor-ed, plus the count.  The same function
+// is restated in oracle/gx_oracle.c (or_state_hash) and statevec.py.
+__device__ __forceinline__ uint64_t dg_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ void digest_flush(unsigned long long c, unsigned long long s,
+                                             unsigned long long x, unsigned long long* out) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        c += __shfl_xor_sync(FULLMASK, c, o);
+        s += __shfl_xor_sync(FULLMASK, s, o);
+        x ^= __shfl_xor_sync(FULLMASK, x, o);
+    }
+    if ((threadIdx.x & 31) == 0 && c) {
+        atomicAdd(&out[0], c);
+        atomicAdd(&out[1], s);
+        atomicXor(&out[2], x);
+    }
+}
+
+// in-band tables (slot j at word j*V): one thread per 16-byte chunk, a
+// streaming pass over the data array
+template <int V>
+__global__ void __launch_bounds__(256) k_digest_mark(TableDesc T, int words, unsigned long long* out) {
+    const uint64_t chunks = T.nb * (uint64_t)T.bw / 4;
+    const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+    unsigned long long c = 0, s = 0, x = 0;
+    const uint4* d = reinterpret_cast<const uint4*>(T.data);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < chunks; i += stride) {
+        const uint4 q = __ldcs(d + i);
+        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int t = 0; t < 4 / V; t++) {
+            if ((w4[t * V + T.mark_word] & T.mark) == 0u) continue;
+            uint64_t h = 0x6A09E667F3BCC908ull ^ (uint64_t)words;
+            for (int w = 0; w < words; w++) {
+                uint32_t y = w4[t * V + w];
+                if (w == (int)T.mark_word) y &= ~T.mark;
+                h = dg_mix(h ^ (uint64_t)y);
+            }
+            c++;
+            s += h;
+            x ^= h;
+        }
+    }
+    digest_flush(c, s, x, out);
+}
+
+// any table: one thread per bucket, slots through the status protocol
+__global__ void __launch_bounds__(256) k_digest_any(TableDesc T, int words, unsigned long long* out) {
+    const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+    unsigned long long c = 0, s = 0, x = 0;
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < T.nb; b += stride) {
+        for (int j = 0; j < (int)T.spb; j++) {
+            if (!slot_occupied(T, b, j)) continue;
+            uint32_t key[GX_MAXV];
+            read_words(T, b, j, key);
+            uint64_t h = 0x6A09E667F3BCC908ull ^ (uint64_t)words;
+            for (int w = 0; w < words; w++) h = dg_mix(h ^ (uint64_t)key[w]);
+            c++;
+            s += h;
+            x ^= h;
+        }
+    }
+    digest_flush(c, s, x, out);
+}
+
 int table_fixup_status(gx_table* t, const uint32_t* d_new_keys, uint64_t n_new) {
     if (!t->d.status) return GX_OK;  // exploration-only table: no statuses to keep
     const TableDesc& T = t->d;
@@ -736,6 +809,30 @@ int gx_read_slots(gx_table* t, const int64_t* handles, uint64_t n, uint8_t* stat
 int gx_dump(gx_table* t, int64_t* handles, uint8_t* status, uint32_t* words, uint64_t cap,
             uint64_t* count) {
     return select_slots(t, 0, t->d.nb, SEL_OCCUPIED, handles, status, words, cap, count);
+}
+
+int gx_table_digest(gx_table* t, int32_t words, uint64_t* out) {
+    const TableDesc& T = t->d;
+    if (words < 1 || words > (int32_t)T.vlen) {
+        set_error("digest over %d words of a %u-word table", words, T.vlen);
+        return GX_EINPUT;
+    }
+    unsigned long long* c = (unsigned long long*)t->d_ctr + CTR_SCRATCH;  // cells 3..5
+    GX_CUDA(cudaMemsetAsync(c, 0, 3 * sizeof(unsigned long long), t->stream));
+    const int grid = sm_count() * 8;
+    const bool inband = T.mode == MODE_MARK && (T.vlen == 1 || T.vlen == 2 || T.vlen == 4);
+    if (inband && T.vlen == 1)
+        k_digest_mark<1><<<grid, 256, 0, t->stream>>>(T, words, c);
+    else if (inband && T.vlen == 2)
+        k_digest_mark<2><<<grid, 256, 0, t->stream>>>(T, words, c);
+    else if (inband)
+        k_digest_mark<4><<<grid, 256, 0, t->stream>>>(T, words, c);
+    else
+        k_digest_any<<<grid, 256, 0, t->stream>>>(T, words, c);
+    GX_LAUNCHED();
+    GX_CUDA(cudaMemcpyAsync(out, c, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, t->stream));
+    GX_CUDA(cudaStreamSynchronize(t->stream));
+    return GX_OK;
 }
 
 }  // extern "C"

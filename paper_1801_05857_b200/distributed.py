@@ -10,10 +10,11 @@ Two drivers share the ownership rule and the level semantics:
 * the collective one (`DeviceShard`, `explore_sharded`, below): expand,
   bin by owner, NCCL all_to_all of counts and payload, insert.
 
-Every rank owns the states whose owner hash (a splitmix finaliser of the
-table's fold value, decorrelated from all bucket indices; gx_device.cuh
-`owner_of`) equals its rank, holds that shard of the state table, and
-expands only its own frontier.  One BFS level:
+Every rank owns the states whose owner hash (a cheap 32-bit murmur-style
+mix of the key words, independent of the table's fold and so decorrelated
+from all bucket indices; gx_device.cuh `key_mix` / `owner_of_mix`) equals
+its rank, holds that shard of the state table, and expands only its own
+frontier.  One BFS level of the collective driver:
 
   1. expand + route   the local frontier's successors are generated on
                       the device and binned by owner (gx_expand_route)
@@ -58,6 +59,7 @@ class ShardResult:
     iterations: int
     outcome: str
     levels: int
+    digest: tuple | None = None  # reachable-set digest over all ranks (gx_table_digest)
 
 
 class DeviceShard:
@@ -161,24 +163,35 @@ class FusedShard:
         from .explore import DeviceNetwork
         from .hashtable import StateTable
 
+        from .explore import device_table_config
         self.rank, self.world = rank, world
         self.scheme = statevec.make_scheme(net)
         self.vlen = statevec.device_vlen(self.scheme, cfg.pad_vlen3)
         self.dnet = DeviceNetwork(net, self.scheme, stream, self.vlen)
-        self.table = StateTable(cfg.table, self.vlen, mark=statevec.mark_bit(self.scheme),
-                                stream=stream, status=status)
+        self.table = StateTable(device_table_config(cfg.table, self.scheme, self.vlen), self.vlen,
+                                mark=statevec.mark_bit(self.scheme, self.vlen), stream=stream,
+                                status=status)
         slots = self.table.total_slots
-        if not frontier_capacity:
+        frontier_capacity = frontier_capacity or cfg.frontier_capacity
+        if not frontier_capacity or not inbox_capacity:
+            # standalone default (one shard per process and GPU): frontier and
+            # inbox together take at most 40% of what this table left free
             sm, free, _tot = device_info()
-            frontier_capacity = max(1 << 16, min(slots + 2, int(free * 0.4) // (4 * self.vlen * world)))
-        if not inbox_capacity:
-            inbox_capacity = frontier_capacity
+            each = max(1 << 16, min(slots + 2, int(free * 0.2) // (4 * self.vlen)))
+            frontier_capacity = frontier_capacity or each
+            inbox_capacity = inbox_capacity or each
         self.frontier_capacity, self.inbox_capacity = frontier_capacity, inbox_capacity
         h = C.c_void_p()
         check(lib().gx_shard_create(self.dnet.handle, self.table.handle, rank, world, inbox_capacity,
                                     frontier_capacity, int(min(cfg.cache_slots, 1 << 30)),
                                     int(cfg.filter_log2), C.byref(h)))
         self._h = h
+        # partitioned dedup levels (in-band tables with 1/2/4-word slots)
+        self.dedup = bool(cfg.dedup) and self.vlen in (1, 2, 4) and self.table.mode == "mark"
+        self.set_slots = 0
+        if self.dedup:
+            check(lib().gx_shard_set_mode(h, 1, int(cfg.dedup_set_log2)))
+            self.set_slots = (1 << int(cfg.dedup_set_log2)) * (2 if self.vlen == 4 else 4)
         self.init = np.zeros(self.vlen, np.uint32)
         packed = statevec.pack(self.scheme, net.initial)
         self.init[:len(packed)] = packed
@@ -236,6 +249,21 @@ class FusedShard:
         from ._lib import check, lib
         check(lib().gx_shard_absorb_chunk(self._h))
 
+    def set_partitions(self, nsub: int):
+        from ._lib import check, lib
+        check(lib().gx_shard_set_partitions(self._h, int(nsub)))
+
+    def chunk_status(self) -> np.ndarray:
+        """[inbox overflow flag, successors routed so far, states expanded so far]"""
+        from ._lib import check, lib, ptr
+        out = np.zeros(3, np.uint64)
+        check(lib().gx_shard_chunk_status(self._h, ptr(out, C.c_uint64)))
+        return out
+
+    def rollback(self):
+        from ._lib import check, lib
+        check(lib().gx_shard_rollback(self._h))
+
     def end_level(self) -> np.ndarray:
         from ._lib import check, lib, ptr
         st = np.zeros(8, np.uint64)
@@ -247,6 +275,10 @@ class FusedShard:
         st = np.zeros(8, np.uint64)
         check(lib().gx_shard_absorb(self._h, ptr(st, C.c_uint64)))
         return st
+
+    def digest(self) -> tuple:
+        """This shard's part of the reachable-set digest (gx_table_digest)."""
+        return self.table.digest(self.scheme.vector_length)
 
     def finish(self):
         from . import statevec
@@ -291,6 +323,8 @@ def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None, redu
     reduce_max = reduce_max or (lambda a: a)
     full = reduce(np.array([sum(int(s.begin(detect)) for s in shards)], np.uint64))[0]
     chunk = min(s.chunk_states for s in shards)
+    dedup = all(getattr(s, "dedup", False) for s in shards)
+    planner = ChunkPlanner(shards) if dedup else None
     rounds = 0
     outcome = "COMPLETE"
     if full:
@@ -298,15 +332,18 @@ def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None, redu
     else:
         while True:
             widest = int(reduce_max(np.array([max(s.frontier() for s in shards)], np.uint64))[0])
-            chunks = max(1, -(-widest // chunk))
-            for c in range(chunks):
-                for s in shards:
-                    s.expand_range(c * chunk, chunk)
-                barrier()
-                for s in shards:
-                    s.absorb_chunk()
-                if c + 1 < chunks:
+            if dedup:
+                _level_partitioned(shards, barrier, reduce, planner, widest)
+            else:
+                chunks = max(1, -(-widest // chunk))
+                for c in range(chunks):
+                    for s in shards:
+                        s.expand_range(c * chunk, chunk)
                     barrier()
+                    for s in shards:
+                        s.absorb_chunk()
+                    if c + 1 < chunks:
+                        barrier()
             st = np.zeros(8, np.uint64)
             for s in shards:
                 st += s.end_level()
@@ -320,7 +357,7 @@ def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None, redu
                 break
             if st[GX_SH["claims"]] == 0:
                 break
-            if max_iterations and rounds >= max_iterations:
+            if max_iterations is not None and rounds >= max_iterations:
                 outcome = "ITERATION_CAP"
                 break
     tot = np.zeros(5, np.uint64)
@@ -335,6 +372,82 @@ def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None, redu
     return tot, sorted(kept)[:100], rounds, outcome, level_ms
 
 
+class ChunkPlanner:
+    """Frontier chunk and sub-partition sizes of the partitioned levels.
+
+    Every shard receives about (states expanded per shard) x (successors
+    per state) keys per chunk; the chunk is sized so that this fills at
+    most 80% of an inbox, from the largest successors-per-state ratio seen
+    so far (initially the network's bound, network.max_successors).  The
+    sub-partition count makes each sub-partition at most twice the dedup
+    set's slots (set load <= 1/2 for >= 4x duplication; less duplication
+    only costs redundant probes).  An overflowing chunk is rolled back and
+    re-run at half the size, so the estimate never affects results."""
+
+    def __init__(self, shards):
+        from .network import max_successors
+        s0 = shards[0]
+        self.world = s0.world
+        self.inbox = min(s.inbox_capacity for s in shards)
+        self.set_slots = min(s.set_slots for s in shards)
+        self.ratio = float(max_successors(s0.dnet.net))
+        self.seen = 0.0
+        self.routed = 0
+        self.expanded = 0
+        self.nsub_max = max(1, min(256, 128 // self.world))
+
+    def chunk(self) -> int:
+        return max(1, int(0.8 * self.inbox / max(self.ratio, 1e-9)))
+
+    def nsub(self, n: int) -> int:
+        keys = n * self.ratio
+        want = max(1, int(-(-keys // (2 * self.set_slots))))
+        p = 1
+        while p < want and p < self.nsub_max:
+            p *= 2
+        return p
+
+    def observe(self, routed: int, expanded: int):
+        dr, de = routed - self.routed, expanded - self.expanded
+        self.routed, self.expanded = routed, expanded
+        if de > 0:
+            self.seen = max(self.seen, dr / de)
+            self.ratio = min(self.ratio, max(1.0, 1.2 * self.seen + 0.5))
+
+    def overflowed(self):
+        self.ratio *= 2.0
+
+
+def _level_partitioned(shards, barrier, reduce, planner, widest: int):
+    """One level of the partitioned dedup engine: frontier chunks of
+    planner.chunk() states per shard; per chunk every shard expands and
+    routes (gx_shard_expand_range), the overflow flags and counters are
+    reduced (the barrier), then every shard filters + probes its
+    sub-partitions (gx_shard_absorb_chunk)."""
+    c = 0
+    while c < widest:
+        n = min(widest - c, planner.chunk())
+        nsub = planner.nsub(n)
+        for s in shards:
+            s.set_partitions(nsub)
+            s.expand_range(c, n)
+        st = np.zeros(3, np.uint64)
+        for s in shards:
+            st += s.chunk_status()
+        st = reduce(st)
+        if st[0]:
+            for s in shards:
+                s.rollback()
+            planner.overflowed()
+            continue
+        planner.observe(int(st[1]), int(st[2]))
+        for s in shards:
+            s.absorb_chunk()
+        c += n
+        if c < widest:
+            barrier()
+
+
 class LocalShardExplorer:
     """`world` hash-owner shards of one network in this process (one GPU),
     built once and explored any number of times (each run clears the
@@ -347,6 +460,11 @@ class LocalShardExplorer:
                  status: bool = True, stream=None):
         self.cfg = cfg
         self.shards = []
+        frontier_capacity = frontier_capacity or cfg.frontier_capacity
+        if not frontier_capacity or not inbox_capacity:
+            f, i = local_buffer_sizes(net, cfg, world, status)
+            frontier_capacity = frontier_capacity or f
+            inbox_capacity = inbox_capacity or i
         try:
             for r in range(world):
                 self.shards.append(FusedShard(net, cfg, r, world, inbox_capacity, frontier_capacity,
@@ -371,12 +489,49 @@ class LocalShardExplorer:
             states=states, transitions=int(tot[1]), deadlocks=tuple(kept),
             deadlocks_total=int(tot[3]), expanded=int(tot[2]), iterations=rounds, wall_time=wall,
             throughput=states / wall if wall > 0 else 0.0, outcome=outcome, probes=int(tot[4]),
-            level_ms=float(level_ms))
+            level_ms=float(level_ms), digest=self.digest() if self.cfg.state_digest else None)
+
+    def digest(self) -> tuple:
+        """The reachable set's digest over all shards (include/gx.h
+        gx_table_digest): equal to one table's for the same set."""
+        return combine_digests(s.digest() for s in self.shards)
 
     def close(self):
         for s in self.shards:
             s.close()
         self.shards = []
+
+
+def combine_digests(parts) -> tuple:
+    """(count, sum, xor) digests of disjoint shards -> the digest of their union."""
+    c = sm = x = 0
+    for pc, ps, px in parts:
+        c += int(pc)
+        sm = (sm + int(ps)) & 0xFFFFFFFFFFFFFFFF
+        x ^= int(px)
+    return c, sm, x
+
+
+def local_buffer_sizes(net, cfg, world: int, status: bool = True):
+    """Default (frontier, inbox) capacities in vectors for `world` shards on
+    this GPU: the tables of ALL shards are budgeted first (each shard's
+    table is cfg.table, padded as device_table_config does), then 40% of the
+    memory they leave is split evenly over the shards' frontiers and
+    inboxes."""
+    from . import statevec
+    from .explore import device_table_config
+    from .hashtable import slots_per_bucket
+    scheme = statevec.make_scheme(net)
+    vlen = statevec.device_vlen(scheme, cfg.pad_vlen3)
+    tc = device_table_config(cfg.table, scheme, vlen)
+    nb = tc.capacity_words // tc.bucket_words
+    spb = slots_per_bucket(tc.bucket_words, vlen, tc.resolved_layout())
+    table_b = nb * (4 * tc.bucket_words + ((((spb + 7) & ~7)) if status else 0))
+    _sm, free, _tot = device_info()
+    left = max(0, free - world * table_b - (256 << 20))
+    each = max(1 << 16, int(left * 0.2) // (world * 4 * vlen))
+    each = min(each, nb * spb + 2)
+    return each, each
 
 
 def explore_local_shards(net, cfg, world: int, inbox_capacity: int = 0, frontier_capacity: int = 0,
@@ -393,7 +548,7 @@ def explore_local_shards(net, cfg, world: int, inbox_capacity: int = 0, frontier
 
 
 def explore_fused(shards, dist, torch, detect: bool, max_iterations=None,
-                  device=None) -> ShardResult:
+                  device=None, digest: bool = True) -> ShardResult:
     """Multi-process driver (one process per GPU, holding one shard or
     several): shards were connected with their peers' IPC handles; the
     barrier and the stats reductions are NCCL all_reduces on the shards'
@@ -415,11 +570,13 @@ def explore_fused(shards, dist, torch, detect: bool, max_iterations=None,
                                                 reduce_max=lambda a: reduce(a, dist.ReduceOp.MAX))
     tot = reduce(tot)
     gathered = [None] * dist.get_world_size()
-    dist.all_gather_object(gathered, kept)
-    dls = tuple(sorted(s for part in gathered for s in part)[:100])
+    mine = [s.digest() for s in shards] if digest else []
+    dist.all_gather_object(gathered, (kept, mine))
+    dls = tuple(sorted(s for part, _ in gathered for s in part)[:100])
+    dig = combine_digests(d for _, ds in gathered for d in ds) if digest else None
     return ShardResult(states=int(tot[0]), transitions=int(tot[1]), deadlocks=dls,
                        deadlocks_total=int(tot[3]), expanded=int(tot[2]), iterations=rounds,
-                       outcome=outcome, levels=rounds - 1)
+                       outcome=outcome, levels=rounds - 1, digest=dig)
 
 
 def connect_fused(shards, dist):
@@ -495,7 +652,7 @@ def explore_sharded(backend, dist, torch, scheme, initial_packed: np.ndarray, de
                 break
             if claims == 0:
                 break
-            if max_iterations and rounds >= max_iterations:
+            if max_iterations is not None and rounds >= max_iterations:
                 outcome = "ITERATION_CAP"
                 break
     st = torch.tensor([backend.states()], dtype=torch.int64, device=dev)

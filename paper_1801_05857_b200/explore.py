@@ -64,6 +64,15 @@ class ExploreConfig:
     # shard.  Keeps each probed table range inside the TLB reach when one
     # table would be tens of GB.  Dumps need shards == 1.
     shards: int = 1
+    # compute the order-independent digest of the reachable set
+    # (gx_table_digest) after the search and put it on the report
+    state_digest: bool = True
+    # sharded engine: partitioned levels with the level-wide duplicate
+    # filter (gx_part.cuh; only the first copy of each successor in a chunk
+    # probes the table) instead of the fused probe-as-you-expand kernels;
+    # the filter set has 2^dedup_set_log2 32-byte groups (L2 resident)
+    dedup: bool = False
+    dedup_set_log2: int = 20
 
     def __post_init__(self):
         if self.workers < 1:
@@ -92,6 +101,9 @@ class ExplorationReport:
     kernels: int = 0
     level_ms: float = 0.0
     probes: int = 0
+    # (count, sum, xor) of the per-state hashes of the reachable set
+    # (include/gx.h gx_table_digest); None when not computed
+    digest: tuple | None = None
 
     def to_dict(self) -> dict:
         return {
@@ -180,13 +192,17 @@ class Explorer:
         self.scheme = statevec.make_scheme(net)
         self.vlen = statevec.device_vlen(self.scheme, cfg.pad_vlen3)
         self.dnet = DeviceNetwork(net, self.scheme, stream, self.vlen)
-        self.table = StateTable(cfg.table, self.vlen,
-                                mark=statevec.mark_bit(self.scheme), stream=stream, status=status)
+        self.table = StateTable(device_table_config(cfg.table, self.scheme, self.vlen), self.vlen,
+                                mark=statevec.mark_bit(self.scheme, self.vlen), stream=stream,
+                                status=status)
         self.last = None
 
     def run(self) -> ExplorationReport:
         cfg = self.cfg
-        ecfg = ExploreCfg(int(cfg.detect_deadlocks), int(cfg.filter_log2), int(cfg.max_iterations or 0),
+        # max_iterations: None = no cap; any integer caps as in the reference
+        # (explore.py:256-261: rounds >= max_iterations, so 0 stops after round 1)
+        cap = -1 if cfg.max_iterations is None else max(0, int(cfg.max_iterations))
+        ecfg = ExploreCfg(int(cfg.detect_deadlocks), int(cfg.filter_log2), cap,
                           int(cfg.frontier_capacity), int(cfg.probe_group),
                           int(min(cfg.cache_slots, 1 << 30)))
         rep = Report()
@@ -206,7 +222,12 @@ class Explorer:
             iterations=int(rep.iterations), wall_time=wall,
             throughput=rep.states / wall if wall > 0 else 0.0, outcome=OUTCOMES[rep.outcome],
             device_ms=float(rep.device_ms), max_frontier=int(rep.max_frontier),
-            kernels=int(rep.kernels), level_ms=float(rep.level_ms), probes=int(rep.probes))
+            kernels=int(rep.kernels), level_ms=float(rep.level_ms), probes=int(rep.probes),
+            digest=self.digest() if cfg.state_digest else None)
+
+    def digest(self) -> tuple:
+        """(count, sum, xor) digest of the reachable set now in the table."""
+        return self.table.digest(self.scheme.vector_length)
 
     def dump_states(self) -> str:
         return statevec.dump_states_array(self.table.dump_arrays()[2][:, :self.scheme.vector_length])
@@ -224,6 +245,26 @@ class Explorer:
     def close(self):
         self.table.close()
         self.dnet.close()
+
+
+def device_table_config(table: TableConfig, scheme, vlen: int) -> TableConfig:
+    """The table geometry for `vlen`-word device slots.  A padded 3-word
+    state (vlen 4) needs more words per slot than the reference's 3, so the
+    bucket count grows until the table has at least the reference's slot
+    count for the same TableConfig (hashtable.py:89-111,155-159): the same
+    number of states fits before TABLE_FULL."""
+    sv = scheme.vector_length
+    if vlen == sv:
+        return table
+    from dataclasses import replace
+
+    from .hashtable import slots_per_bucket
+    layout = table.resolved_layout()
+    bw = table.bucket_words
+    ref_slots = (table.capacity_words // bw) * slots_per_bucket(bw, sv, layout)
+    spb = slots_per_bucket(bw, vlen, layout)
+    buckets = -(-ref_slots // spb)
+    return replace(table, capacity_words=max(buckets, 1) * bw)
 
 
 def explore(net: Network, cfg: ExploreConfig, dump_states=None, dump_table=None):

@@ -268,6 +268,14 @@ class StateTable:
                                 C.byref(cnt)))
         return hs[:n], st[:n], ws[:n]
 
+    def digest(self, words: int | None = None) -> tuple:
+        """(count, sum, xor) of the per-state hashes of the occupied slots'
+        first `words` words (include/gx.h gx_table_digest); order- and
+        placement-independent, so shards and engines compare exactly."""
+        out = np.zeros(3, np.uint64)
+        check(lib().gx_table_digest(self._h, int(words or self.vector_length), ptr(out, C.c_uint64)))
+        return int(out[0]), int(out[1]), int(out[2])
+
     def occupied_vectors(self) -> list:
         return [tuple(int(x) for x in row) for row in self.dump_arrays()[2]]
 

@@ -115,9 +115,13 @@ def device_vlen(scheme: PackingScheme, pad: bool = True) -> int:
     return 4 if (pad and v == 3) else v
 
 
-def mark_bit(scheme: PackingScheme):
+def mark_bit(scheme: PackingScheme, vlen: int | None = None):
     """(word, bit) of a bit no packed state ever sets -- the top bit of the
-    word with the most unused bits -- or None if every word is full."""
+    word with the most unused bits -- or None if every word is full.  With
+    device padding (vlen > the scheme's), the always-zero padding word's top
+    bit."""
+    if vlen is not None and vlen > scheme.vector_length:
+        return vlen - 1, WORD_BITS - 1
     used = [0] * scheme.vector_length
     for w, sh, width in zip(scheme.word_index, scheme.shift, scheme.widths):
         used[w] = max(used[w], sh + width)
@@ -125,3 +129,38 @@ def mark_bit(scheme: PackingScheme):
     if used[best] >= WORD_BITS:
         return None
     return best, WORD_BITS - 1
+
+
+# ------------------------------------------------------------ set digest
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _mix64(z: np.ndarray) -> np.ndarray:
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def state_hashes(words: np.ndarray) -> np.ndarray:
+    """Per-state hash of packed vectors (n, vlen) u32 (include/gx.h
+    gx_table_digest): h = 0x6A09E667F3BCC908 ^ vlen, then h = mix64(h ^ w)
+    for each word."""
+    words = np.asarray(words, np.uint32)
+    words = words.reshape(len(words), -1) if words.ndim != 2 else words
+    h = np.full(len(words), 0x6A09E667F3BCC908 ^ words.shape[1], np.uint64)
+    with np.errstate(over="ignore"):
+        for j in range(words.shape[1]):
+            h = _mix64(h ^ words[:, j].astype(np.uint64))
+    return h
+
+
+def state_digest(words: np.ndarray) -> tuple:
+    """(count, sum mod 2^64, xor) of state_hashes: the order-independent
+    multiset digest of a set of packed states."""
+    h = state_hashes(words)
+    if len(h) == 0:
+        return 0, 0, 0
+    s = int(np.sum(h, dtype=np.uint64))
+    x = int(np.bitwise_xor.reduce(h))
+    return len(h), s, x
+

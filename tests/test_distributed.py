@@ -256,6 +256,9 @@ class OracleFusedShard:
         self._level_reset()
         return st
 
+    def digest(self):
+        return self.base.table.digest(self.vlen)
+
     def finish(self):
         class Rep:
             pass
@@ -270,11 +273,15 @@ def _fused_worker(rank, world, port, jobs, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1801_05857_b200.distributed import explore_fused
     out = []
-    for name, table_kw, max_it in jobs:
-        s = OracleFusedShard(model_path(name), table_kw, world, rank)
-        r = explore_fused(s, dist, torch, True, max_iterations=max_it, device=torch.device("cpu"))
-        out.append((name, r.states, r.transitions, r.iterations, r.deadlocks_total,
-                    tuple(map(tuple, r.deadlocks)), r.outcome, r.expanded))
+    try:
+        for name, table_kw, max_it in jobs:
+            s = OracleFusedShard(model_path(name), table_kw, world, rank)
+            r = explore_fused(s, dist, torch, True, max_iterations=max_it, device=torch.device("cpu"))
+            out.append((name, r.states, r.transitions, r.iterations, r.deadlocks_total,
+                        tuple(map(tuple, r.deadlocks)), r.outcome, r.expanded, r.digest))
+    except Exception as err:  # noqa: BLE001 - surfaced to the parent
+        q.put(repr(err))
+        raise
     if rank == 0:
         q.put(out)
     dist.barrier()
@@ -297,14 +304,17 @@ def test_fused_driver_matches_single_process():
         for p in procs:
             p.start()
         res = q.get(timeout=600)
+        assert not isinstance(res, str), res
         for p in procs:
             p.join(timeout=120)
             assert p.exitcode == 0
-        for (name, states, trans, iters, dl_total, dls, outcome, expanded), job in zip(res, jobs):
+        for (name, states, trans, iters, dl_total, dls, outcome, expanded, dig), job in zip(res, jobs):
             ref = O.explore(O.Net.from_file(model_path(name)), capacity_words=job[1]["capacity_words"],
                             detect_deadlocks=True, max_iterations=job[2])
             assert (states, trans, iters, dl_total, outcome, expanded) == \
                 (ref.states, ref.transitions, ref.iterations, ref.deadlocks_total, ref.outcome,
                  ref.expanded), (name, world)
+            if outcome == "COMPLETE":
+                assert dig == ref.table.digest(), (name, world)
             if job[2] is None:
                 assert sorted(map(list, dls)) == sorted(models[name]["bfs"]["deadlocks"])[:100], name

@@ -17,6 +17,7 @@ from paper_1801_05857_b200.explore import DeviceNetwork, ExploreConfig, Explorer
 from paper_1801_05857_b200.hashtable import StateTable, TableConfig  # noqa: E402
 
 MODELS = golden_models()
+REF_DIGESTS = json.loads((GOLDEN / "ref_digests.json").read_text())
 
 
 def sha(text):
@@ -216,6 +217,8 @@ def test_explore_matches_reference(name):
                    "iterations": rep.iterations, "outcome": rep.outcome}
             assert got == want, (name, run["table"])
             assert sha(dump) == run["dump_states_sha"], (name, run["table"])
+            if rep.outcome == "COMPLETE":
+                assert list(rep.digest) == REF_DIGESTS[name], (name, run["table"])
             hs, st, _ = ex.table.dump_arrays()
             occ, new, _ = ex.table.occupancy()
             assert occ == rep.states and new == int((st == 2).sum())
