@@ -76,6 +76,9 @@ def parse():
                     help="per-block shared-memory dedup cache entries (< 32 = off)")
     ap.add_argument("--filter-log2", type=int, default=0,
                     help="GPU-wide L2 dedup filter of 2^k entries (0 = off)")
+    ap.add_argument("--dedup", action="store_true",
+                    help="sharded engine: partitioned levels with the level-wide L2 duplicate filter")
+    ap.add_argument("--dedup-set-log2", type=int, default=20)
     ap.add_argument("--cpu-sample", default="ring12")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hash-bench", action="store_true",
@@ -404,7 +407,8 @@ def main():
     tcfg = TableConfig(bucket_words=args.bucket_words, num_hash_functions=args.hash_functions,
                        capacity_words=cap)
     cfg = ExploreConfig(table=tcfg, detect_deadlocks=True, probe_group=args.probe_group,
-                        cache_slots=max(1, args.cache_slots), filter_log2=args.filter_log2)
+                        cache_slots=max(1, args.cache_slots), filter_log2=args.filter_log2,
+                        dedup=args.dedup, dedup_set_log2=args.dedup_set_log2, state_digest=False)
     stream = torch.cuda.current_stream().cuda_stream
     from paper_1801_05857_b200.hashtable import slots_per_bucket
     spb0 = slots_per_bucket(args.bucket_words, vlen, "half" if args.bucket_words == 32 else "plain")
@@ -427,7 +431,8 @@ def main():
         # never more than what the tables and frontiers leave free
         left = torch.cuda.mem_get_info()[0] - cap * 4 * shards - status_bytes * status \
             - front * 4 * vlen * shards
-        inbox = max(1 << 20, min(inbox, int(0.85 * left) // (4 * vlen * shards)))
+        # the partitioned mode also holds a quarter-inbox buffer of first occurrences
+        inbox = max(1 << 20, min(inbox, int(0.85 * left) // (4 * vlen * shards * (5 if args.dedup else 4) // 4)))
         ex = LocalShardExplorer(net, cfg, shards, inbox_capacity=inbox, frontier_capacity=front,
                                 status=status, stream=stream)
         total_slots = sum(sh.table.total_slots for sh in ex.shards)

@@ -43,8 +43,8 @@ __device__ __forceinline__ uint32_t part_bin(uint32_t x, int world, uint32_t nsu
 }
 
 struct PartArgs {
-    uint32_t nsub;       // sub-partitions per shard this chunk
-    uint32_t pad;
+    uint32_t nsub;       // sub-partitions per shard this chunk (a power of two)
+    uint32_t sub_log2;   // log2(nsub)
     uint64_t cap_sub;    // keys per sub-partition
 };
 
@@ -92,9 +92,9 @@ __device__ __forceinline__ void route_partitioned(const TableDesc& T, const Rout
         const uint32_t b = b0 + lane;
         const uint32_t c = b < nbins ? hist[b] : 0u;
         unsigned long long g = 0;
+        const uint32_t o = b >> P.sub_log2, sb = b & (P.nsub - 1);
         if (c) {
-            const uint32_t o = b / P.nsub, s = b % P.nsub;
-            g = atomicAdd(R.inbox_ctr[o] + s, (unsigned long long)c);
+            g = atomicAdd(R.inbox_ctr[o] + sb, (unsigned long long)c);
             if (g + c > P.cap_sub) atomicExch(ovf, 1ull);
         }
         uint32_t incl = c;
@@ -105,8 +105,13 @@ __device__ __forceinline__ void route_partitioned(const TableDesc& T, const Rout
         }
         __syncwarp();
         if (b < nbins) {
-            base[b] = g;
-            hist[b] = run + incl - c;  // hist now holds the sorted start of bin b
+            const uint32_t start = run + incl - c;
+            hist[b] = start;  // hist now holds the sorted start of bin b
+            // base[b]: slot of sorted position 0 of bin b (mod 2^64: it may
+            // lie below 0, only positions >= start are used; |value| < 2^62),
+            // or 2^63 when the bin overflows its sub-partition
+            base[b] = g + c > P.cap_sub ? (1ull << 63) : (unsigned long long)sb * P.cap_sub + g - start;
+            (void)o;
         }
         run += __shfl_sync(FULLMASK, incl, 31);
     }
@@ -124,10 +129,9 @@ __device__ __forceinline__ void route_partitioned(const TableDesc& T, const Rout
     // pass 3: consecutive sorted keys -> consecutive partition slots
     for (uint32_t e = lane; e < m; e += 32) {
         const uint32_t b = sbin[e];
-        const uint64_t slot = base[b] + (e - hist[b]);
-        if (slot < P.cap_sub) {
-            const uint32_t o = b / P.nsub, s = b % P.nsub;
-            uint32_t* dst = R.inbox[o] + ((uint64_t)s * P.cap_sub + slot) * V;
+        const unsigned long long bb = base[b];
+        if (bb != (1ull << 63)) {
+            uint32_t* dst = R.inbox[b >> P.sub_log2] + (bb + e) * V;
             if (V == 2) {
                 *reinterpret_cast<uint2*>(dst) = make_uint2(sq[e * 2], sq[e * 2 + 1]);
             } else if (V == 4) {
@@ -302,6 +306,72 @@ __device__ __forceinline__ bool dedup_first(void* set, uint32_t groups, const ui
         if (old == k) return false;     // another copy won the race
     }
     return true;  // group full: probe (redundant at worst)
+}
+
+// dedup_first for KPL keys per lane with all their group loads in flight
+// at once, then all needed CASes back to back, then the verdicts (a CAS
+// lost to another key re-runs dedup_first for that key alone, out of
+// line).  first[i] in: key i is live; out: it is the first occurrence.
+template <int V>
+__device__ __noinline__ bool dedup_retry(void* set, uint32_t groups, const uint32_t* km) {
+    return dedup_first<V>(set, groups, km);
+}
+
+template <int V, int KPL>
+__device__ __forceinline__ void dedup_batch(void* set, uint32_t groups, const uint32_t (&km)[KPL][V],
+                                            bool (&first)[KPL]) {
+    using S = DedupSlot<V>;
+    using W = typename S::W;
+    if constexpr (V == 4) {  // 128-bit slots: one key at a time
+#pragma unroll
+        for (int i = 0; i < KPL; i++)
+            if (first[i]) first[i] = dedup_retry<V>(set, groups, km[i]);
+        return;
+    }
+    const uint4* base = reinterpret_cast<const uint4*>(set);
+    uint32_t gi[KPL];
+    uint4 a[KPL], b[KPL];
+#pragma unroll
+    for (int i = 0; i < KPL; i++) {
+        uint32_t x[V];
+#pragma unroll
+        for (int w = 0; w < V; w++) x[w] = km[i][w];
+        gi[i] = dedup_index(key_mix<V>(x), groups);
+        a[i] = b[i] = make_uint4(0, 0, 0, 0);
+        if (first[i]) {
+            a[i] = __ldcg(base + 2 * (uint64_t)gi[i]);
+            b[i] = __ldcg(base + 2 * (uint64_t)gi[i] + 1);
+        }
+    }
+    const uint32_t hi_w = V == 2 ? 1 : 0;
+    int cand[KPL];
+#pragma unroll
+    for (int i = 0; i < KPL; i++) {
+        const uint32_t k0 = km[i][0], k1 = V == 2 ? km[i][hi_w % V] : 0u;
+        const bool s0 = a[i].x == k0 && a[i].y == k1, s1 = a[i].z == k0 && a[i].w == k1;
+        const bool s2 = b[i].x == k0 && b[i].y == k1, s3 = b[i].z == k0 && b[i].w == k1;
+        const bool e0 = (a[i].x | a[i].y) == 0u, e1 = (a[i].z | a[i].w) == 0u;
+        const bool e2 = (b[i].x | b[i].y) == 0u, e3 = (b[i].z | b[i].w) == 0u;
+        cand[i] = e0 ? 0 : e1 ? 1 : e2 ? 2 : e3 ? 3 : -1;
+        if (s0 || s1 || s2 || s3) {
+            first[i] = false;
+            cand[i] = -1;
+        }
+        if (!first[i]) cand[i] = -1;
+    }
+    W old[KPL];
+#pragma unroll
+    for (int i = 0; i < KPL; i++) {
+        old[i] = 0;
+        if (cand[i] >= 0)
+            old[i] = atomicCAS(reinterpret_cast<W*>(set) + 4 * (uint64_t)gi[i] + cand[i], (W)0, S::word(km[i]));
+    }
+#pragma unroll
+    for (int i = 0; i < KPL; i++) {
+        if (cand[i] < 0 || old[i] == (W)0) continue;  // decided / installed: first
+        if (old[i] == S::word(km[i])) first[i] = false;
+        else first[i] = dedup_retry<V>(set, groups, km[i]);  // lost the slot to another key
+    }
 }
 
 }  // namespace gx

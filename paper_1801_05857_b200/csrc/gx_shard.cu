@@ -39,7 +39,18 @@ __global__ void __launch_bounds__(256, GX_STAGED_MINB) k_level_routed(TableDesc 
 // the next frontier through the level's LevelArgs.
 template <int BW, int V>
 __global__ void __launch_bounds__(256, GX_STAGED_MINB) k_absorb(TableDesc T, LevelArgs A, const uint32_t* __restrict__ inbox,
-                                                  const unsigned long long* count, uint64_t cap) {
+                                                  const unsigned long long* count, uint64_t cap,
+                                                  const unsigned long long* use_alt = nullptr,
+                                                  const uint32_t* __restrict__ alt = nullptr,
+                                                  const unsigned long long* alt_count = nullptr,
+                                                  uint64_t alt_cap = 0) {
+    // partitioned mode: when the duplicate filter's output overflowed
+    // (*use_alt), absorb the unfiltered sub-partition instead
+    if (use_alt && *use_alt) {
+        inbox = alt;
+        count = alt_count;
+        cap = alt_cap;
+    }
     using L = StagedSmem<BW, V>;
     using S = Staged<BW, V>;
     constexpr int QCAP = QWORDS / V;
@@ -86,107 +97,101 @@ __global__ void __launch_bounds__(256, 2) k_level_part(TableDesc T, NetDesc N, L
     level_part_body<V>(T, N, A, R, P);
 }
 
-// K2: one sub-partition of this shard: drop keys already seen in this chunk
-// (L2 set), FINDORPUT the first occurrences, append the inserted to the
-// next frontier.  Keys arrive with the mark bit set.
-template <int BW, int V>
-__global__ void __launch_bounds__(256, GX_STAGED_MINB) k_absorb_dedup(TableDesc T, LevelArgs A,
-                                                                      const uint32_t* __restrict__ keys,
-                                                                      const unsigned long long* count,
-                                                                      uint64_t cap, void* set, uint32_t groups) {
-    using L = StagedSmem<BW, V>;
-    using S = Staged<BW, V>;
-    constexpr int QCAP = QWORDS / V;
+// K2a: one sub-partition of this shard through the L2 duplicate filter:
+// the first occurrence of each key in the chunk is appended (mark bit
+// cleared) to uniq; k_absorb then FINDORPUTs uniq (K2b).  No shared
+// memory, so many more warps keep set lookups in flight than the probe
+// kernel could.  Keys arrive with the mark bit set.
+template <int V>
+__global__ void __launch_bounds__(256, 4) k_dedup(TableDesc T, const uint32_t* __restrict__ keys,
+                                                  const unsigned long long* count, uint64_t cap, void* set,
+                                                  uint32_t groups, uint32_t* uniq, unsigned long long* uniq_ctr,
+                                                  uint64_t uniq_cap, unsigned long long* ovf) {
     constexpr int KPL = 4;  // keys per lane with their set lookups in flight
-    extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
-    const int wid = threadIdx.x >> 5;
-    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * QWORDS;
-    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::KB;
-    uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
     const uint64_t n = min((uint64_t)*count, cap);
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-    unsigned long long probes = 0;
     const uint32_t unmark = ~T.mark;
-    for (uint64_t base = warp * QCAP; base < n; base += nwarps * QCAP) {
-        const uint32_t m0 = (uint32_t)min((uint64_t)QCAP, n - base);
-        uint32_t kept = 0;
-        for (uint32_t r0 = 0; r0 < m0; r0 += 32 * KPL) {
-            uint32_t km[KPL][V];
-            bool first[KPL];
+    for (uint64_t base = warp * (32 * KPL); base < n; base += nwarps * (32 * KPL)) {
+        uint32_t km[KPL][V];
+        bool first[KPL];
 #pragma unroll
-            for (int i = 0; i < KPL; i++) {
-                const uint32_t e = r0 + i * 32 + lane;
-                const bool a = e < m0;
-                if (a) {
-                    if (V == 2) {
-                        const uint2 x = __ldcs(reinterpret_cast<const uint2*>(keys + (base + e) * 2));
-                        km[i][0] = x.x;
-                        km[i][1 % V] = x.y;
-                    } else if (V == 4) {
-                        const uint4 x = __ldcs(reinterpret_cast<const uint4*>(keys + (base + e) * 4));
-                        km[i][0] = x.x;
-                        km[i][1 % V] = x.y;
-                        km[i][2 % V] = x.z;
-                        km[i][3 % V] = x.w;
-                    } else {
-#pragma unroll
-                        for (int w = 0; w < V; w++) km[i][w] = __ldcs(keys + (base + e) * V + w);
-                    }
+        for (int i = 0; i < KPL; i++) {
+            const uint64_t e = base + i * 32 + lane;
+            const bool a = e < n;
+            if (a) {
+                if (V == 2) {
+                    const uint2 x = __ldcs(reinterpret_cast<const uint2*>(keys + e * 2));
+                    km[i][0] = x.x;
+                    km[i][1 % V] = x.y;
+                } else if (V == 4) {
+                    const uint4 x = __ldcs(reinterpret_cast<const uint4*>(keys + e * 4));
+                    km[i][0] = x.x;
+                    km[i][1 % V] = x.y;
+                    km[i][2 % V] = x.z;
+                    km[i][3 % V] = x.w;
                 } else {
 #pragma unroll
-                    for (int w = 0; w < V; w++) km[i][w] = 0u;
+                    for (int w = 0; w < V; w++) km[i][w] = __ldcs(keys + e * V + w);
                 }
-                bool marked = false;  // a written slot carries the mark bit
+            } else {
 #pragma unroll
-                for (int w = 0; w < V; w++) marked |= (km[i][w] & (w == (int)T.mark_word ? T.mark : 0u)) != 0u;
-                first[i] = a && marked;
+                for (int w = 0; w < V; w++) km[i][w] = 0u;
             }
+            bool marked = false;  // a written slot carries the mark bit
 #pragma unroll
-            for (int i = 0; i < KPL; i++)
-                if (first[i]) first[i] = dedup_first<V>(set, groups, km[i]);
-#pragma unroll
-            for (int i = 0; i < KPL; i++) {
-                const uint32_t msk = __ballot_sync(FULLMASK, first[i]);
-                if (first[i]) {
-                    const uint32_t p = kept + __popc(msk & lanemask_lt());
-#pragma unroll
-                    for (int w = 0; w < V; w++) q[p * V + w] = w == (int)T.mark_word ? (km[i][w] & unmark) : km[i][w];
-                }
-                kept += __popc(msk);
-            }
+            for (int w = 0; w < V; w++) marked |= (km[i][w] & (w == (int)T.mark_word ? T.mark : 0u)) != 0u;
+            first[i] = a && marked;
         }
-        __syncwarp();
-        probes += lane == 0 ? kept : 0;
-        uint32_t full = 0;
-        const uint32_t n_out = probe_staged<BW, V>(T, q, kept, stage, sbkt, &full);
-        if (__any_sync(FULLMASK, full != 0u) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
-        if (n_out) flush_out<V>(A, q, n_out);
-        __syncwarp();
+        dedup_batch<V, KPL>(set, groups, km, first);
+        uint32_t msk[KPL], tot = 0;
+#pragma unroll
+        for (int i = 0; i < KPL; i++) {
+            msk[i] = __ballot_sync(FULLMASK, first[i]);
+            tot += __popc(msk[i]);
+        }
+        if (!tot) continue;
+        unsigned long long pos = 0;
+        if (lane == 0) pos = atomicAdd(uniq_ctr, (unsigned long long)tot);
+        pos = __shfl_sync(FULLMASK, pos, 0);
+        if (pos + tot > uniq_cap) {
+            if (lane == 0) atomicExch(ovf, 1ull);
+            continue;
+        }
+#pragma unroll
+        for (int i = 0; i < KPL; i++) {
+            if (first[i]) {
+                uint32_t* d = uniq + (pos + __popc(msk[i] & lanemask_lt())) * V;
+#pragma unroll
+                for (int w = 0; w < V; w++) d[w] = w == (int)T.mark_word ? (km[i][w] & unmark) : km[i][w];
+            }
+            pos += __popc(msk[i]);
+        }
     }
-    probes = warp_sum(probes);
-    if (lane == 0 && probes) atomicAdd(&A.ctr[LV_PROBES], probes);
 }
 
 typedef void (*part_kernel_t)(TableDesc, NetDesc, LevelArgs, RouteArgs, PartArgs);
-typedef void (*dedup_kernel_t)(TableDesc, LevelArgs, const uint32_t*, const unsigned long long*, uint64_t,
-                               void*, uint32_t);
+typedef void (*dedup_kernel_t)(TableDesc, const uint32_t*, const unsigned long long*, uint64_t, void*, uint32_t,
+                               uint32_t*, unsigned long long*, uint64_t, unsigned long long*);
+typedef void (*absorb2_kernel_t)(TableDesc, LevelArgs, const uint32_t*, const unsigned long long*, uint64_t,
+                                 const unsigned long long*, const uint32_t*, const unsigned long long*, uint64_t);
 
 struct PartKernels {
-    part_kernel_t a;
-    dedup_kernel_t b;
-    size_t smem_a, smem_b;
+    part_kernel_t a;     // K1: expand + route
+    dedup_kernel_t b;    // K2a: duplicate filter
+    absorb2_kernel_t c;  // K2b: FINDORPUT of the first occurrences
+    size_t smem_a, smem_c;
 };
 
 template <int BW>
 static PartKernels pick_part_v(int v) {
     switch (v) {
-        case 1: return {k_level_part<1>, k_absorb_dedup<BW, 1>, PartSmem<1>::FIXED, StagedSmem<BW, 1>::FIXED};
-        case 2: return {k_level_part<2>, k_absorb_dedup<BW, 2>, PartSmem<2>::FIXED, StagedSmem<BW, 2>::FIXED};
-        case 4: return {k_level_part<4>, k_absorb_dedup<BW, 4>, PartSmem<4>::FIXED, StagedSmem<BW, 4>::FIXED};
+        case 1: return {k_level_part<1>, k_dedup<1>, k_absorb<BW, 1>, PartSmem<1>::FIXED, StagedSmem<BW, 1>::FIXED};
+        case 2: return {k_level_part<2>, k_dedup<2>, k_absorb<BW, 2>, PartSmem<2>::FIXED, StagedSmem<BW, 2>::FIXED};
+        case 4: return {k_level_part<4>, k_dedup<4>, k_absorb<BW, 4>, PartSmem<4>::FIXED, StagedSmem<BW, 4>::FIXED};
     }
-    return {nullptr, nullptr, 0, 0};
+    return {nullptr, nullptr, nullptr, 0, 0};
 }
 
 static PartKernels pick_part(const TableDesc& T) {
@@ -196,11 +201,12 @@ static PartKernels pick_part(const TableDesc& T) {
         case 16: return pick_part_v<16>((int)T.vlen);
         case 32: return pick_part_v<32>((int)T.vlen);
     }
-    return {nullptr, nullptr, 0, 0};
+    return {nullptr, nullptr, nullptr, 0, 0};
 }
 
 typedef void (*routed_kernel_t)(TableDesc, NetDesc, LevelArgs, RouteArgs);
-typedef void (*absorb_kernel_t)(TableDesc, LevelArgs, const uint32_t*, const unsigned long long*, uint64_t);
+typedef void (*absorb_kernel_t)(TableDesc, LevelArgs, const uint32_t*, const unsigned long long*, uint64_t,
+                                const unsigned long long*, const uint32_t*, const unsigned long long*, uint64_t);
 
 struct ShardKernels {
     routed_kernel_t a;
@@ -279,6 +285,8 @@ struct gx_shard {
     DevBuf set;
     uint32_t set_groups = 0;
     DevBuf snap;  // level counters before the current chunk's expansion (rollback)
+    DevBuf uniq;  // first occurrences of one sub-partition: [ctr, ovf, pad..256 B][keys]
+    uint64_t uniq_cap = 0;
     size_t smem_a = 0;
 };
 
@@ -363,6 +371,7 @@ int gx_shard_destroy(gx_shard* s) {
     s->gf.release();
     s->set.release();
     s->snap.release();
+    s->uniq.release();
     for (cudaEvent_t e : s->ev) cudaEventDestroy(e);
     delete s;
     return GX_OK;
@@ -541,7 +550,13 @@ int gx_shard_set_mode(gx_shard* s, int32_t dedup, int32_t set_log2) {
         s->smem_a = (P.smem_a + 15) & ~size_t(15);
     }
     GX_CUDA(cudaFuncSetAttribute((const void*)P.a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->smem_a));
-    GX_CUDA(cudaFuncSetAttribute((const void*)P.b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_b));
+    GX_CUDA(cudaFuncSetAttribute((const void*)P.c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_c));
+    // first occurrences of a sub-partition: a quarter of the inbox (more
+    // only below 4x duplication; then the unfiltered sub-partition is
+    // absorbed instead, decided on the device)
+    s->uniq_cap = std::max<uint64_t>(s->inbox_cap / 4, 1 << 16);
+    rc = s->uniq.ensure(256 + sizeof(uint32_t) * T.vlen * s->uniq_cap);
+    if (rc) return rc;
     s->dedup = true;
     s->nsub = 1;
     s->cap_sub = s->inbox_cap;
@@ -549,8 +564,8 @@ int gx_shard_set_mode(gx_shard* s, int32_t dedup, int32_t set_log2) {
 }
 
 int gx_shard_set_partitions(gx_shard* s, uint32_t nsub) {
-    if (nsub < 1 || nsub > GX_PART_SUB_MAX || (uint64_t)nsub * s->world > GX_PART_BINS_MAX) {
-        set_error("%u sub-partitions x %d shards outside the routing limits (%d per shard, %d bins)", nsub,
+    if (nsub < 1 || nsub > GX_PART_SUB_MAX || (nsub & (nsub - 1)) || (uint64_t)nsub * s->world > GX_PART_BINS_MAX) {
+        set_error("%u sub-partitions x %d shards: need a power of two within %d per shard, %d bins", nsub,
                   s->world, GX_PART_SUB_MAX, GX_PART_BINS_MAX);
         return GX_EINPUT;
     }
@@ -577,7 +592,7 @@ int gx_shard_expand_range(gx_shard* s, uint64_t begin, uint64_t count) {
         if (count) {
             PartArgs P;
             P.nsub = s->nsub;
-            P.pad = 0;
+            P.sub_log2 = (uint32_t)__builtin_ctz(s->nsub);
             P.cap_sub = s->cap_sub;
             A.cache_mask = s->smem_a > ((s->P.smem_a + 15) & ~size_t(15)) && s->cslots ? s->cslots - 1 : 0;
             const uint64_t want = (count + 31) / 32;
@@ -639,11 +654,19 @@ int gx_shard_absorb_chunk(gx_shard* s) {
         const uint32_t* keys = (const uint32_t*)((char*)s->inbox_block + INBOX_HEAD);
         cudaEvent_t b0 = next_event(s), b1 = next_event(s);
         GX_CUDA(cudaEventRecord(b0, st));
+        unsigned long long* uctr = (unsigned long long*)s->uniq.p;  // [0] count, [1] overflow
+        uint32_t* ukeys = (uint32_t*)((char*)s->uniq.p + 256);
+        LevelArgs A = s->A;
+        A.cache_mask = 0;
         for (uint32_t sub = 0; sub < s->nsub; sub++) {
+            const uint32_t* skeys = keys + (uint64_t)sub * s->cap_sub * t->d.vlen;
             GX_CUDA(cudaMemsetAsync(s->set.p, 0, 32ull * s->set_groups, st));
-            s->P.b<<<sm_count() * GX_STAGED_MINB, 256, s->P.smem_b, st>>>(
-                t->d, s->A, keys + (uint64_t)sub * s->cap_sub * t->d.vlen, cur + sub, s->cap_sub, s->set.p,
-                s->set_groups);
+            GX_CUDA(cudaMemsetAsync(uctr, 0, 16, st));
+            s->P.b<<<sm_count() * 4, 256, 0, st>>>(t->d, skeys, cur + sub, s->cap_sub, s->set.p, s->set_groups,
+                                                   ukeys, uctr, s->uniq_cap, uctr + 1);
+            GX_LAUNCHED();
+            s->P.c<<<sm_count() * GX_STAGED_MINB, 256, s->P.smem_c, st>>>(t->d, A, ukeys, uctr, s->uniq_cap,
+                                                                         uctr + 1, skeys, cur + sub, s->cap_sub);
             GX_LAUNCHED();
         }
         GX_CUDA(cudaEventRecord(b1, st));
@@ -656,7 +679,8 @@ int gx_shard_absorb_chunk(gx_shard* s) {
     cudaEvent_t b0 = next_event(s), b1 = next_event(s);
     GX_CUDA(cudaEventRecord(b0, st));
     s->K.b<<<sm_count() * GX_STAGED_MINB, 256, s->smem, st>>>(t->d, s->A, s->R.inbox[s->rank],
-                                                             s->R.inbox_ctr[s->rank], s->inbox_cap);
+                                                             s->R.inbox_ctr[s->rank], s->inbox_cap, nullptr,
+                                                             nullptr, nullptr, 0);
     GX_LAUNCHED();
     GX_CUDA(cudaEventRecord(b1, st));
     GX_CUDA(cudaMemsetAsync(s->R.inbox_ctr[s->rank], 0, 8, st));
