@@ -45,6 +45,7 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 TLB_REACH = 60 << 30    # one table beyond this: shard it on the GPU (profiles/README.md)
 SHARD_BYTES = 80 << 30  # table bytes per shard at most (ring19 sweep: 2 x 79 GB > 3 x 52 GB > 4 x 39 GB)
 TRAFFIC = ROOT / "profiles" / "traffic.json"
+GOLDEN_DIGESTS = ROOT / "tests" / "golden" / "digests.json"
 METRIC = "states explored/sec"
 
 
@@ -79,11 +80,14 @@ def parse():
     ap.add_argument("--dedup", action="store_true",
                     help="sharded engine: partitioned levels with the level-wide L2 duplicate filter")
     ap.add_argument("--dedup-set-log2", type=int, default=20)
-    ap.add_argument("--cpu-sample", default="ring12")
+    ap.add_argument("--cpu-sample", default="ring14",
+                    help="token ring the CPU reference arm explores (ring14: 4.5e7 states, ~12 s on 16 cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hash-bench", action="store_true",
                     help="skip the isolated hash-table sweeps (configs[1])")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--crosscheck", type=int, default=1,
+                    help="sharded headline: re-explore once on one table and assert the same digest")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the configs[2] (peterson6) and ring16 side measurements")
     return ap.parse_args()
@@ -170,6 +174,36 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def cpu_hash_baseline(total: int = 1 << 22):
+    """run_insert_bench's CPU counterpart (reference bench.py:120-202 with
+    threads=1): the reference's table restated in C
+    (oracle/gx_oracle.c find_or_insert, one thread) inserting a
+    duplication sequence of `total` one-word keys, per bucket size and
+    d in {1, 10, 100}; the table sized as insert_bench_table_config."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_1801_05857_b200.bench import DuplicationSpec, insert_bench_table_config
+    rows = []
+    for bw in (4, 8, 16, 32):
+        for d in (1, 10, 100):
+            spec = DuplicationSpec(total=total, duplication=d, vector_length=1)
+            cfg = insert_bench_table_config(spec, bw)
+            rng = np.random.default_rng(11)
+            u = total // d
+            keys = rng.integers(0, 1 << 32, size=u, dtype=np.uint64).astype(np.uint32)
+            seq = keys[np.minimum(rng.permutation(total) // d, u - 1)]
+            t = O.Table(bw, 8, cfg.capacity_words, None, 42, 1)
+            t0 = time.perf_counter()
+            codes, _ = t.find_or_insert_batch(seq)
+            dt = time.perf_counter() - t0
+            rows.append({"bw": bw, "d": d, "ops": total, "ops_per_sec": total / dt,
+                         "inserted": int((codes == 1).sum())})
+    return {"kind": "port", "cores": 1, "unit": "FINDORPUT ops/s", "rows": rows,
+            "sample": f"{total} one-word keys per cell, oracle/gx_oracle.c table (hashtable.py:224-280 "
+                      "restated), 1 thread, K=8, table sized for <= 50% load at d=1"}
+
+
 def cpu_reference(sample: str, steps: int, warmup: int, tmp: Path):
     """The reference engine's C port on all host threads, bounded sample."""
     from oracle import oracle as O
@@ -231,11 +265,16 @@ def hash_sweep(ra: dict):
     """Isolated FINDORPUT throughput vs bucket size and fill (configs[1],
     SURVEY §8(d) protocol 2): a 32 GiB table of 2-word vectors (>> L2;
     1-word keys have only 2^31 distinct values next to the mark bit, too
-    few to fill it) filled step by step with fresh random keys; at each
-    fill f the next 2^28 inserts and a lookup pass over the same keys are
-    timed.  K = 8 (the reference default) and K = 32
-    (fill >= 0.6 needs it).  Algorithmic bytes per op:
-    4 (key) + S(bw) (bucket) + 32 if inserted; frac against R(S(bw))."""
+    few to fill it) filled step by step with fresh random keys.  At each
+    fill f: an untimed fill to f - 2%, then a timed insert batch of 2% of
+    the slots (8.6e7 ops at bw 32, 6.9e7 at bw 4: 2^28 inserts would move
+    the fill by ~6%), then a timed lookup batch of 2^28 FINDORPUTs of keys
+    already present (the last 2^28 rows inserted).  K = 8 (the reference
+    default) and K = 32 (fill >= 0.6 needs it).  Keys are
+    generated inside the kernel, so the algorithmic bytes per op are the
+    bucket probe S(bw) (+ one 32-byte sector written per insert); extra
+    buckets probed past the first are reported (buckets_per_op) but not
+    credited.  frac against R(S(bw)) measured in the same run."""
     from paper_1801_05857_b200.bench import device_insert_bench
     from paper_1801_05857_b200.hashtable import StateTable, TableConfig
     out = []
@@ -246,24 +285,32 @@ def hash_sweep(ra: dict):
             t = StateTable(TableConfig(bucket_words=bw, num_hash_functions=k, capacity_words=words),
                            2, mark=(1, 31))
             slots = t.total_slots
-            done = 0
+            rows = 0  # rows attempted so far: the next fresh keys start here
             for fill in (0.5, 0.6, 0.7, 0.8, 0.9):
                 target = int(fill * slots)
-                batch = min(1 << 28, int(0.02 * slots))
-                if target - batch > done:  # untimed fill to (fill - 2%)
-                    r = device_insert_bench(t, target - batch - done, 1, seed=7, row_base=done)
-                    done += r["inserted"]
+                batch = int(0.02 * slots)
+                occ = t.occupancy()[0]
+                if target - batch > occ:  # untimed fill to (fill - 2%)
+                    n = target - batch - occ
+                    r = device_insert_bench(t, n, 1, seed=7, row_base=rows)
+                    rows += n
                     if r["full"]:
-                        out.append({"bw": bw, "k": k, "fill": fill, "table_full": True})
+                        out.append({"vlen": 2, "bw": bw, "k": k, "fill": fill, "table_full": True})
                         break
-                r = device_insert_bench(t, batch, 1, seed=7, row_base=done)
-                done += r["inserted"]
-                look = device_insert_bench(t, batch, 1, seed=7, row_base=done - batch)
-                ins_gbs = r["ops_per_sec"] * (8 + s_bw(bw) + 32) / 1e9
-                look_gbs = look["ops_per_sec"] * (8 + s_bw(bw)) / 1e9
+                r = device_insert_bench(t, batch, 1, seed=7, row_base=rows)
+                rows += batch
+                nl = min(1 << 28, rows)
+                look = device_insert_bench(t, nl, 1, seed=7, row_base=rows - nl)
+                assert look["inserted"] == 0 or r["full"], look  # every looked-up key is present
+                ins_gbs = r["ops_per_sec"] * (s_bw(bw) + 32) / 1e9
+                look_gbs = look["ops_per_sec"] * s_bw(bw) / 1e9
                 out.append({"vlen": 2, "bw": bw, "k": k, "fill": fill,
+                            "fill_after": t.occupancy()[0] / slots,
+                            "insert_ops": batch, "lookup_ops": nl,
                             "insert_ops_per_sec": r["ops_per_sec"],
                             "lookup_ops_per_sec": look["ops_per_sec"],
+                            "insert_buckets_per_op": r["buckets_per_op"],
+                            "lookup_buckets_per_op": look["buckets_per_op"],
                             "insert_gbs_alg": ins_gbs, "lookup_gbs_alg": look_gbs,
                             "lookup_frac_of_random_roofline": look_gbs / r_g if r_g else None,
                             "table_full": bool(r["full"])})
@@ -275,11 +322,15 @@ def hash_sweep(ra: dict):
 
 def duplication_sweep(ra: dict):
     """The paper's Fig. 4 protocol (bench.py:90-114,120-202): 2^30 FINDORPUT
-    ops (n >= 2^30) over total/d unique random vectors, globally shuffled, table sized
-    for <= 50% load at d = 1; bucket 4 ("Gh-cbs") vs 32 ("Gh"), 1-word
-    vectors (the paper's) and 2-word ones.  A cell whose
-    sizing overfills the buckets reports table_full (vlen 2 at bw 4: 2
-    slots per bucket at 50% load, as in the reference)."""
+    ops (n >= 2^30) over total/d unique random vectors,
+    globally shuffled, table sized for <= 50% load at d = 1; bucket 4
+    ("Gh-cbs") vs 32 ("Gh"), 1-word vectors (the paper's) and 2-word ones
+    (SURVEY §8(d)).  Keys are generated inside the kernel: algorithmic
+    bytes per op = S(bw) + 32 per insert.  The reference's checks hold:
+    inserted == total // d and inserted == occupancy (bench.py:176-190).  A
+    cell whose sizing overfills the buckets reports table_full (vlen 2 at
+    bw 4: 2 slots per bucket at 50% load, as in the reference, SURVEY
+    B.4)."""
     from paper_1801_05857_b200.bench import (DuplicationSpec, device_insert_bench,
                                              insert_bench_table_config)
     from paper_1801_05857_b200.hashtable import StateTable
@@ -292,46 +343,66 @@ def duplication_sweep(ra: dict):
                 t = StateTable(insert_bench_table_config(spec, bw), vlen, mark=(vlen - 1, 31))
                 try:
                     r = device_insert_bench(t, total, d, seed=11)
+                    occ = t.occupancy()[0]
                 finally:
                     t.close()
                 u = total // d
-                alg = (total * (4 * vlen + s_bw(bw)) + u * 32) / (r["ms"] / 1e3) / 1e9
+                if not r["full"]:
+                    assert r["inserted"] == u == occ and r["found"] == total - u, (vlen, bw, d, r, occ)
+                alg = (total * s_bw(bw) + u * 32) / (r["ms"] / 1e3) / 1e9
                 r_g = ra.get(s_bw(bw), {}).get("gbs")
                 out.append({"vlen": vlen, "bw": bw, "d": d, "ops_per_sec": r["ops_per_sec"],
-                            "inserted": r["inserted"], "found": r["found"], "gbs_alg": alg,
+                            "inserted": r["inserted"], "found": r["found"], "occupancy": occ,
+                            "buckets_per_op": r["buckets_per_op"], "gbs_alg": alg,
                             "frac_of_random_roofline": alg / r_g if r_g else None,
                             "table_full": bool(r["full"])})
     return out
 
 
-def extra_workloads(torch, tmp: Path):
-    """Side measurements on one table (not the headline): configs[2], a
-    peterson7-class model (Peterson's filter lock with 6 processes, ~1e8
-    states), and ring16 (8 GB table), each 1 warm-up + 2 timed runs."""
+def single_table_rate(torch, name: str, tmp: Path, runs: int = 2) -> dict:
+    """states/s of ringN / gasN / petersonN on one table (the explore()
+    engine), CUDA events over `runs` explorations after one warm-up; the
+    digest is checked against tests/golden/digests.json when present."""
     import paper_1801_05857_b200 as gx
     from paper_1801_05857_b200.explore import ExploreConfig, Explorer
     from paper_1801_05857_b200.hashtable import TableConfig
+    golden = json.loads(GOLDEN_DIGESTS.read_text()).get(name, {}) if GOLDEN_DIGESTS.exists() else {}
+    states = golden.get("states") or (closed_form(name) or (1 << 24,))[0]
+    net = gx.load_network(model_path(name, tmp))
+    from paper_1801_05857_b200 import statevec
+    v = statevec.device_vlen(statevec.make_scheme(net))
+    cfg = ExploreConfig(table=TableConfig(capacity_words=table_capacity(states, v, 32, 0.5),
+                                          num_hash_functions=16), detect_deadlocks=True, state_digest=False)
+    ex = Explorer(net, cfg, stream=torch.cuda.current_stream().cuda_stream)
+    ex.run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    reps = [ex.run() for _ in range(runs)]
+    e1.record()
+    torch.cuda.synchronize()
+    r = reps[-1]
+    d = list(ex.digest())
+    ex.close()
+    ms = e0.elapsed_time(e1) / runs
+    ok = None
+    if golden.get("digest"):
+        ok = d == golden["digest"] and r.transitions == golden["transitions"]
+        assert ok, (name, d, golden)
+    return {"workload": name, "states": r.states, "transitions": r.transitions, "levels": r.iterations - 1,
+            "ms_per_exploration": ms, "states_per_sec": r.states / (ms / 1e3), "digest_ok": ok}
+
+
+def extra_workloads(torch, tmp: Path):
+    """Side measurements on one table (not the headline): configs[2], a
+    peterson7-class model (Peterson's filter lock with 6 processes, 2.1e8
+    states), and ring16 (8 GB table), each 1 warm-up + 2 timed runs, their
+    reachable sets checked against the golden digests."""
     out = []
-    for name, words, k in (("peterson6", 1 << 31, 16), ("ring16", table_capacity(459165024, 2, 32, 0.5), 8)):
-        net = gx.load_network(model_path(name, tmp))
-        cfg = ExploreConfig(table=TableConfig(capacity_words=words, num_hash_functions=k),
-                            detect_deadlocks=True)
-        ex = Explorer(net, cfg, stream=torch.cuda.current_stream().cuda_stream)
-        ex.run()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record()
-        reps = [ex.run() for _ in range(2)]
-        e1.record()
-        torch.cuda.synchronize()
-        ex.close()
-        r = reps[-1]
-        assert r.outcome == "COMPLETE" and reps[0].states == r.states
-        ms = e0.elapsed_time(e1) / 2
-        out.append({"workload": ("configs[2] " if name.startswith("peterson") else "") + name,
-                    "states": r.states, "transitions": r.transitions, "levels": r.iterations - 1,
-                    "table_bytes": words * 4, "ms_per_exploration": ms,
-                    "states_per_sec": r.states / (ms / 1e3)})
+    for name in ("peterson6", "ring16"):
+        r = single_table_rate(torch, name, tmp)
+        r["workload"] = ("configs[2] " if name.startswith("peterson") else "") + name
+        out.append(r)
     return out
 
 
@@ -466,13 +537,39 @@ def main():
     alg_bytes = rep.transitions * sbw + rep.states * 12 * vlen
     level_ms = statistics.mean(r.level_ms for r in reps)
     achieved = alg_bytes / (level_ms / 1e3) / 1e9
+    # probe-based bytes: the probes actually issued (self-loops are never
+    # probed, block-cache hits skip theirs) plus the inbox round trip of
+    # the successors routed to another shard
+    routed = getattr(rep, "routed", 0) or 0
+    probe_bytes = rep.probes * sbw + rep.states * 12 * vlen + routed * 8 * vlen
     traffic = None
     if TRAFFIC.exists():
         tr = json.loads(TRAFFIC.read_text())
         key = f"{args.workload}/bw{args.bucket_words}/shards{shards}"
         if key in tr:  # DRAM bytes of one exploration's level kernels (ncu, profiles/)
             traffic = tr[key]["bytes_per_step"]
+    # set identity of the timed run: its digest against the golden one
+    # (tests/golden/digests.json: the oracle's / the closed-form
+    # enumeration of the reachable set, data only)
+    digest = list(ex.digest())
+    golden = json.loads(GOLDEN_DIGESTS.read_text()).get(args.workload, {}) if GOLDEN_DIGESTS.exists() else {}
+    if golden.get("digest"):
+        assert digest == golden["digest"], (digest, golden["digest"])
     ex.close()
+    crosscheck = None
+    if shards > 1 and args.crosscheck:
+        # the same model on ONE table (the single-GPU engine): same set
+        t0 = time.perf_counter()
+        one = TableConfig(bucket_words=args.bucket_words, num_hash_functions=args.hash_functions,
+                          capacity_words=table_capacity(states_est, vlen, args.bucket_words, args.load))
+        ex1 = Explorer(net, ExploreConfig(table=one, detect_deadlocks=True, state_digest=False),
+                       stream=stream, status=False)
+        r1 = ex1.run()
+        d1 = list(ex1.digest())
+        ex1.close()
+        assert (r1.states, r1.transitions, d1) == (rep.states, rep.transitions, digest), (r1, d1, digest)
+        crosscheck = {"engine": "single table (gx_explore)", "states": r1.states, "transitions": r1.transitions,
+                      "digest": d1, "equal": True, "seconds": time.perf_counter() - t0}
 
     # the random-access roofline R(g) on this GPU: a 32 GiB buffer (>> L2,
     # inside the TLB reach) and, for tables beyond the reach, the table size
@@ -508,9 +605,19 @@ def main():
     e2e_value = r.states * len(e2e_times) / sum(e2e_times) if e2e_times else None
 
     cpu = None
+    same = None
+    hash_cpu = None
     if not args.no_cpu_baseline and rank == 0:
-        cpu = cpu_reference(args.cpu_sample, 2, 1, tmp)
+        cpu = cpu_reference(args.cpu_sample, 1, 0, tmp)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        # the GPU on the CPU's own sample: a same-workload pair
+        gpu_same = single_table_rate(torch, args.cpu_sample, tmp)
+        same = {"workload": args.cpu_sample, "gpu_states_per_sec": gpu_same["states_per_sec"],
+                "cpu_states_per_sec": cpu["value"], "cpu_cores": cpu["cores"],
+                "gpu_over_cpu": gpu_same["states_per_sec"] / cpu["value"],
+                "gpu_engine": "single table, explore() engine", "digest_ok": gpu_same["digest_ok"]}
+        if not args.no_hash_bench:
+            hash_cpu = cpu_hash_baseline()
 
     line = {
         "metric": METRIC, "value": value, "unit": "states/s", "n_gpus": 1,
@@ -536,11 +643,20 @@ def main():
                      "kernel": "k_level_staged" if shards == 1 else "k_level_routed + k_absorb",
                      "algorithmic_bytes_per_step": alg_bytes,
                      "kernel_ms_per_step": level_ms,
-                     "bytes_model": "transitions*max(32,4*bw) + states*12*vlen",
+                     "bytes_model": "transitions*max(32,4*bw) + states*12*vlen (SURVEY §8(d))",
+                     "probe_bytes_per_step": probe_bytes,
+                     "probe_bytes_model": "probes*max(32,4*bw) + states*12*vlen + routed*8*vlen "
+                                          "(probes actually issued; inbox write + read)",
+                     "achieved_probe_based": probe_bytes / (level_ms / 1e3) / 1e9,
+                     "frac_probe_based": probe_bytes / (level_ms / 1e3) / 1e9 / hbm_peak,
                      "random_access_gbs": r_peak,
                      "frac_of_random_access": achieved / r_peak,
                      "random_access": ra, "random_access_table_size": ra_table},
         "cpu_baseline": cpu,
+        "same_workload_cpu_vs_gpu": same,
+        "digest": {"value": digest, "golden": golden.get("digest"),
+                   "golden_source": golden.get("source"), "equal": digest == golden.get("digest")},
+        "engine_crosscheck": crosscheck,
         "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": csr_bytes,
                 "d2h_bytes_per_step": 64 + 400 * vlen,
                 "api": "paper_1801_05857_b200.explore(net, cfg) (allocates + frees the table)"
@@ -548,6 +664,7 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "probes_per_step": rep.probes,
+        "routed_per_step": routed,
         "step_breakdown_ms": {"level_kernels": level_ms,
                               "level_loop": statistics.mean(r.device_ms for r in reps) if shards == 1
                               else None,
@@ -555,7 +672,8 @@ def main():
                               "max_frontier": rep.max_frontier},
     }
     if not args.no_hash_bench:
-        line["hash_bench"] = {"fill_sweep": hash_sweep(ra), "duplication_sweep": duplication_sweep(ra)}
+        line["hash_bench"] = {"fill_sweep": hash_sweep(ra), "duplication_sweep": duplication_sweep(ra),
+                              "cpu_baseline": hash_cpu}
     if not args.no_extra:
         line["extra_workloads"] = extra_workloads(torch, tmp)
     print(json.dumps(line), flush=True)

@@ -113,6 +113,12 @@ int gx_find_or_put(gx_table *t, const uint32_t *keys, uint64_t n, uint8_t *codes
 int gx_find_or_put_device(gx_table *t, const uint32_t *d_keys, uint64_t n, uint8_t *d_codes,
                           int64_t *d_handles, uint64_t *inserted, uint64_t *full);
 
+/* gx_find_or_put (concurrent, not serial) with the FINDORPUT kernel timed
+ * alone by CUDA events in *kernel_ms (key upload and code download
+ * excluded): run_insert_bench's timed region (bench.py:120-202 times only
+ * the insert loop). */
+int gx_find_or_put_timed(gx_table *t, const uint32_t *keys, uint64_t n, uint8_t *codes, double *kernel_ms);
+
 /* claim_new (hashtable.py:296-313): claimed[i] = 1 iff this call moved
  * handles[i] NEW -> OLD.  Repeated handles in one batch: exactly one wins. */
 int gx_claim_new(gx_table *t, const int64_t *handles, uint64_t n, uint8_t *claimed);
@@ -322,10 +328,12 @@ int gx_bench_find_or_put(gx_table *t, uint64_t total, uint64_t duplication, uint
                          uint64_t *inserted, uint64_t *full);
 
 /* Same, with the unique rows numbered from row_base (so successive calls
- * can fill a table step by step with fresh keys: the fill-factor sweep). */
+ * can fill a table step by step with fresh keys: the fill-factor sweep);
+ * *loads (may be NULL) = bucket loads issued (probe_group 0 only), so
+ * loads / total is the mean number of buckets a FINDORPUT touched. */
 int gx_bench_find_or_put_rows(gx_table *t, uint64_t total, uint64_t duplication, uint64_t row_base,
                               uint64_t seed, int32_t key_bits, int32_t probe_group, double *ms,
-                              uint64_t *found, uint64_t *inserted, uint64_t *full);
+                              uint64_t *found, uint64_t *inserted, uint64_t *full, uint64_t *loads);
 
 /* Random-access HBM roofline R(g) (SURVEY.md §8(d) denominator; no
  * reference counterpart): `reads` aligned random reads of `granularity`

@@ -71,6 +71,7 @@ SIGNATURES = {
     "gx_table_mode": (C.c_int, [_vp]),
     "gx_find_or_put": (C.c_int, [_vp, _u32p, C.c_uint64, _u8p, _i64p, C.c_int32]),
     "gx_find_or_put_device": (C.c_int, [_vp, _vp, C.c_uint64, _vp, _vp, _u64p, _u64p]),
+    "gx_find_or_put_timed": (C.c_int, [_vp, _u32p, C.c_uint64, _u8p, _P(C.c_double)]),
     "gx_claim_new": (C.c_int, [_vp, _i64p, C.c_uint64, _u8p]),
     "gx_scan_new": (C.c_int, [_vp, C.c_uint64, C.c_uint64, _i64p, C.c_uint64, _u64p]),
     "gx_occupancy": (C.c_int, [_vp, _u64p, _u64p]),
@@ -90,7 +91,7 @@ SIGNATURES = {
                                        _P(C.c_double), _u64p, _u64p, _u64p]),
     "gx_bench_find_or_put_rows": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                             C.c_int32, C.c_int32, _P(C.c_double), _u64p, _u64p,
-                                            _u64p]),
+                                            _u64p, _u64p]),
     "gx_random_access_bench": (C.c_int, [C.c_uint64, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
                                          _P(C.c_double), _P(C.c_double)]),
     "gx_shard_create": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_uint64, C.c_uint64, C.c_int32,

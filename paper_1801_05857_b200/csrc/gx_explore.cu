@@ -545,7 +545,7 @@ __device__ __forceinline__ void bench_row(uint64_t r, int kb, uint64_t seed, uin
 struct BenchArgs {
     uint64_t total, dup, unique, row_base, seed;
     int32_t key_bits, perm_bits_n;
-    unsigned long long* ctr;  // [0] inserted, [1] full
+    unsigned long long* ctr;  // [0] inserted, [1] full, [2] bucket loads (staged kernel)
 };
 
 template <int V>
@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(256, 2) k_bench_staged(TableDesc T, BenchArgs 
                                             (size_t)wid * S::STAGE_BYTES);
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-    unsigned long long ins = 0, full = 0;
+    unsigned long long ins = 0, full = 0, loads = 0;
     for (uint64_t base = warp * KB; base < B.total; base += nwarps * KB) {
         const uint32_t m = (uint32_t)min((uint64_t)KB, B.total - base);
         for (uint32_t k = lane; k < m; k += 32) {
@@ -639,17 +639,20 @@ __global__ void __launch_bounds__(256, 2) k_bench_staged(TableDesc T, BenchArgs 
             for (int w = 0; w < V; w++) q[k * V + w] = key[w];
         }
         __syncwarp();
-        uint32_t f = 0;
-        const uint32_t n_ins = probe_staged<BW, V>(T, q, m, stage, sbkt, &f);
+        uint32_t f = 0, np = 0;
+        const uint32_t n_ins = probe_staged<BW, V>(T, q, m, stage, sbkt, &f, &np);
         ins += lane == 0 ? n_ins : 0;
         full += f;  // keys that hit TABLE_FULL
+        loads += np;
         __syncwarp();
     }
     ins = warp_sum(ins);
     full = warp_sum(full);
+    loads = warp_sum(loads);
     if (lane == 0) {
         if (ins) atomicAdd(&B.ctr[0], ins);
         if (full) atomicAdd(&B.ctr[1], full);
+        if (loads) atomicAdd(&B.ctr[2], loads);
     }
 }
 
@@ -1316,12 +1319,13 @@ int gx_owner_of(const gx_table* t, const uint32_t* keys, uint64_t n, int32_t ran
 int gx_bench_find_or_put(gx_table* t, uint64_t total, uint64_t dup, uint64_t seed, int32_t key_bits,
                          int32_t group, double* ms, uint64_t* found, uint64_t* inserted,
                          uint64_t* full) {
-    return gx_bench_find_or_put_rows(t, total, dup, 0, seed, key_bits, group, ms, found, inserted, full);
+    return gx_bench_find_or_put_rows(t, total, dup, 0, seed, key_bits, group, ms, found, inserted, full,
+                                     nullptr);
 }
 
 int gx_bench_find_or_put_rows(gx_table* t, uint64_t total, uint64_t dup, uint64_t row_base,
                               uint64_t seed, int32_t key_bits, int32_t group, double* ms,
-                              uint64_t* found, uint64_t* inserted, uint64_t* full) {
+                              uint64_t* found, uint64_t* inserted, uint64_t* full, uint64_t* loads) {
     if (total == 0 || dup == 0 || dup > total || key_bits < 1 || key_bits > 32) {
         set_error("bad benchmark parameters");
         return GX_EINPUT;
@@ -1346,7 +1350,7 @@ int gx_bench_find_or_put_rows(gx_table* t, uint64_t total, uint64_t dup, uint64_
     }
     cudaStream_t st = t->stream;
     unsigned long long* c = (unsigned long long*)t->d_ctr + CTR_SCRATCH;
-    GX_CUDA(cudaMemsetAsync(c, 0, 2 * sizeof(unsigned long long), st));
+    GX_CUDA(cudaMemsetAsync(c, 0, 3 * sizeof(unsigned long long), st));
     BenchArgs B;
     B.total = total;
     B.dup = dup;
@@ -1369,9 +1373,10 @@ int gx_bench_find_or_put_rows(gx_table* t, uint64_t total, uint64_t dup, uint64_
     k<<<sm_count() * std::max(resident, 1), 256, BK.smem, st>>>(T, B);
     GX_LAUNCHED();
     GX_CUDA(cudaEventRecord(e1, st));
-    unsigned long long h[2];
+    unsigned long long h[3];
     GX_CUDA(cudaMemcpyAsync(h, c, sizeof h, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaStreamSynchronize(st));
+    if (loads) *loads = BK.smem ? h[2] : 0;  // counted by the staged kernel only
     float f = 0;
     GX_CUDA(cudaEventElapsedTime(&f, e0, e1));
     cudaEventDestroy(e0);

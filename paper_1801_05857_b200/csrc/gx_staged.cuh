@@ -132,7 +132,7 @@ struct Staged {
 template <int BW, int V, int KBX = 0>
 __device__ __forceinline__ uint32_t probe_staged(const TableDesc& T, uint32_t* q, uint32_t m,
                                                  uint4* stage, unsigned long long* sbkt,
-                                                 uint32_t* full) {
+                                                 uint32_t* full, uint32_t* nprobe = nullptr) {
     using S = Staged<BW, V, KBX>;
     constexpr int KB = S::KB, KPL = S::KPL, CH = S::CH, SPC = S::SPC;
     constexpr unsigned long long SKIP = ~0ull;
@@ -168,6 +168,7 @@ __device__ __forceinline__ uint32_t probe_staged(const TableDesc& T, uint32_t* q
                 bkt[i] = pend[i] ? bucket_of(T, h[i], hi) : 0;
                 sbkt[k] = pend[i] ? bkt[i] : SKIP;
                 any |= pend[i];
+                if (nprobe) *nprobe += pend[i] ? 1u : 0u;  // bucket loads (the bench's probes/op)
             }
             if (!__any_sync(FULLMASK, any)) break;
             __syncwarp();

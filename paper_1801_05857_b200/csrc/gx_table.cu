@@ -730,6 +730,31 @@ int gx_find_or_put(gx_table* t, const uint32_t* keys, uint64_t n, uint8_t* codes
     return GX_OK;
 }
 
+int gx_find_or_put_timed(gx_table* t, const uint32_t* keys, uint64_t n, uint8_t* codes, double* kernel_ms) {
+    if (kernel_ms) *kernel_ms = 0.0;
+    if (n == 0) return GX_OK;
+    const uint64_t v = t->d.vlen;
+    int rc = t->keys.ensure(sizeof(uint32_t) * n * v);
+    if (!rc) rc = t->codes.ensure(n);
+    if (rc) return rc;
+    GX_CUDA(cudaMemcpyAsync(t->keys.p, keys, sizeof(uint32_t) * n * v, cudaMemcpyHostToDevice, t->stream));
+    cudaEvent_t e0, e1;
+    GX_CUDA(cudaEventCreate(&e0));
+    GX_CUDA(cudaEventCreate(&e1));
+    GX_CUDA(cudaEventRecord(e0, t->stream));
+    rc = table_find_or_put_dev(t, (const uint32_t*)t->keys.p, n, (uint8_t*)t->codes.p, nullptr, 0, 0);
+    GX_CUDA(cudaEventRecord(e1, t->stream));
+    if (codes) GX_CUDA(cudaMemcpyAsync(codes, t->codes.p, n, cudaMemcpyDeviceToHost, t->stream));
+    GX_CUDA(cudaStreamSynchronize(t->stream));
+    float ms = 0;
+    GX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc) return rc;
+    if (kernel_ms) *kernel_ms = ms;
+    return GX_OK;
+}
+
 int gx_find_or_put_device(gx_table* t, const uint32_t* d_keys, uint64_t n, uint8_t* d_codes,
                           int64_t* d_handles, uint64_t* inserted, uint64_t* full) {
     unsigned long long before[CTR_N];

@@ -60,6 +60,7 @@ class ShardResult:
     outcome: str
     levels: int
     digest: tuple | None = None  # reachable-set digest over all ranks (gx_table_digest)
+    routed: int = 0  # successors routed to another shard's inbox (all ranks)
 
 
 class DeviceShard:
@@ -326,6 +327,7 @@ def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None, redu
     dedup = all(getattr(s, "dedup", False) for s in shards)
     planner = ChunkPlanner(shards) if dedup else None
     rounds = 0
+    routed = 0
     outcome = "COMPLETE"
     if full:
         outcome = "TABLE_FULL"
@@ -348,6 +350,7 @@ def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None, redu
             for s in shards:
                 st += s.end_level()
             st = reduce(st)
+            routed = int(st[GX_SH["routed"]])
             rounds += 1
             if st[GX_SH["overflow"]]:
                 raise RuntimeError("frontier capacity exceeded in sharded exploration; "
@@ -369,7 +372,7 @@ def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None, redu
                         np.uint64)
         level_ms += rep.level_ms
         kept.extend(k)
-    return tot, sorted(kept)[:100], rounds, outcome, level_ms
+    return tot, sorted(kept)[:100], rounds, outcome, level_ms, routed
 
 
 class ChunkPlanner:
@@ -480,16 +483,17 @@ class LocalShardExplorer:
         from .explore import ExplorationReport
 
         t0 = time.perf_counter()
-        tot, kept, rounds, outcome, level_ms = _run_levels(self.shards, lambda: None, lambda a: a,
-                                                           self.cfg.detect_deadlocks,
-                                                           self.cfg.max_iterations)
+        tot, kept, rounds, outcome, level_ms, routed = _run_levels(self.shards, lambda: None, lambda a: a,
+                                                                   self.cfg.detect_deadlocks,
+                                                                   self.cfg.max_iterations)
         wall = time.perf_counter() - t0
         states = int(tot[0])
         return ExplorationReport(
             states=states, transitions=int(tot[1]), deadlocks=tuple(kept),
             deadlocks_total=int(tot[3]), expanded=int(tot[2]), iterations=rounds, wall_time=wall,
             throughput=states / wall if wall > 0 else 0.0, outcome=outcome, probes=int(tot[4]),
-            level_ms=float(level_ms), digest=self.digest() if self.cfg.state_digest else None)
+            level_ms=float(level_ms), routed=routed,
+            digest=self.digest() if self.cfg.state_digest else None)
 
     def digest(self) -> tuple:
         """The reachable set's digest over all shards (include/gx.h
@@ -566,8 +570,8 @@ def explore_fused(shards, dist, torch, detect: bool, max_iterations=None,
         dist.all_reduce(t, op=op or dist.ReduceOp.SUM)
         return t.cpu().numpy().astype(np.uint64)
 
-    tot, kept, rounds, outcome, _ = _run_levels(list(shards), barrier, reduce, detect, max_iterations,
-                                                reduce_max=lambda a: reduce(a, dist.ReduceOp.MAX))
+    tot, kept, rounds, outcome, _, routed = _run_levels(list(shards), barrier, reduce, detect, max_iterations,
+                                                        reduce_max=lambda a: reduce(a, dist.ReduceOp.MAX))
     tot = reduce(tot)
     gathered = [None] * dist.get_world_size()
     mine = [s.digest() for s in shards] if digest else []
@@ -576,7 +580,7 @@ def explore_fused(shards, dist, torch, detect: bool, max_iterations=None,
     dig = combine_digests(d for _, ds in gathered for d in ds) if digest else None
     return ShardResult(states=int(tot[0]), transitions=int(tot[1]), deadlocks=dls,
                        deadlocks_total=int(tot[3]), expanded=int(tot[2]), iterations=rounds,
-                       outcome=outcome, levels=rounds - 1, digest=dig)
+                       outcome=outcome, levels=rounds - 1, digest=dig, routed=routed)
 
 
 def connect_fused(shards, dist):

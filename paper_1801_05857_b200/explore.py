@@ -104,6 +104,8 @@ class ExplorationReport:
     # (count, sum, xor) of the per-state hashes of the reachable set
     # (include/gx.h gx_table_digest); None when not computed
     digest: tuple | None = None
+    # sharded engine: successors stored into another shard's inbox
+    routed: int = 0
 
     def to_dict(self) -> dict:
         return {

@@ -344,3 +344,47 @@ def test_cli_explore_json(capsys):
         assert (doc["states"], doc["transitions"], doc["deadlocks_total"], doc["outcome"]) == \
             (b["states"], b["transitions"], b["deadlocks_total"], "COMPLETE")
         assert doc["config"]["bucket_words"] == 32
+
+
+@pytest.mark.parametrize("bw", [4, 8, 16, 32])
+@pytest.mark.parametrize("vlen", [1, 2])
+def test_device_bench_reference_pins(bw, vlen):
+    """The on-device duplication benchmark (the configs[1] numbers) counts
+    exactly: found=4500 inserted=500 at (5000, d=10) (reference
+    tests/test_cli.py:140-148), 47619 unique at (10^6, d=21)
+    (tests/test_bench.py:37-39), and inserted == total // d == occupancy
+    (bench.py:176-190) at every duplication."""
+    from paper_1801_05857_b200.bench import (DuplicationSpec, device_insert_bench,
+                                             insert_bench_table_config)
+    for total, d in ((5000, 10), (10 ** 6, 21), (1 << 20, 1), (10 ** 6, 100), (3 << 20, 7)):
+        spec = DuplicationSpec(total=total, duplication=d, vector_length=vlen)
+        t = StateTable(insert_bench_table_config(spec, bw), vlen, mark=(vlen - 1, 31))
+        try:
+            r = device_insert_bench(t, total, d, seed=11)
+            occ = t.occupancy()[0]
+        finally:
+            t.close()
+        if r["full"]:  # vlen 2 at bw 4: 2 slots per bucket at 50% load (SURVEY B.4)
+            assert bw == 4 and vlen == 2
+            continue
+        assert (r["found"], r["inserted"], occ) == (total - total // d, total // d, total // d), (total, d)
+        if (total, d) == (5000, 10):
+            assert (r["found"], r["inserted"]) == (4500, 500)
+        if (total, d) == (10 ** 6, 21):
+            assert r["inserted"] == 47619
+
+
+def test_run_insert_bench_and_cli_pins(tmp_path, capsys):
+    """run_insert_bench on the reference's sequence semantics and the CLI's
+    `bench-hash --total 5000 --dup 10` line (tests/test_cli.py:140-148)."""
+    from paper_1801_05857_b200.bench import DuplicationSpec, insert_bench_table_config, run_insert_bench
+    from paper_1801_05857_b200.cli import main
+    spec = DuplicationSpec(total=10 ** 6, duplication=21)
+    rec = run_insert_bench(spec, insert_bench_table_config(spec, 32))
+    assert (rec.inserted_count, rec.found_count) == (47619, 10 ** 6 - 47619)
+    assert rec.wall_ms > 0
+    rc = main(["bench-hash", "--total", "5000", "--dup", "10", "--reps", "1", "--csv",
+               str(tmp_path / "b.csv")])
+    assert rc == 0
+    assert "found=4500 inserted=500" in capsys.readouterr().out
+    assert (tmp_path / "b.csv").exists()
