@@ -436,13 +436,28 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
+        # NCCL's init lines (communicator size, transports) on stderr, so the
+        # JSON line on stdout stays the only stdout output
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if oversub:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_1801_05857_b200.distributed import bench_sharded
+        peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
+        golden = json.loads(GOLDEN_DIGESTS.read_text()).get(args.workload) if GOLDEN_DIGESTS.exists() else None
+
+        def cpu_fn():
+            if args.no_cpu_baseline:
+                return None
+            with tempfile.TemporaryDirectory() as td:
+                c = cpu_reference(args.cpu_sample, 1, 0, Path(td))
+            return {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
         line = bench_sharded(args, torch, dist, model_path, closed_form, table_capacity,
-                             ClockSampler(local))
+                             ClockSampler(local), cpu_fn=cpu_fn, peaks=peaks, golden=golden)
         if oversub:
             line["config"]["oversubscribed"] = (f"{world} ranks on {torch.cuda.device_count()} GPU(s); "
                                                 "gloo counters")

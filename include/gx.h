@@ -305,6 +305,21 @@ int gx_shard_expand_range(gx_shard *s, uint64_t begin, uint64_t count);
  * any shard overflowed, every shard calls gx_shard_rollback (the chunk's
  * counters and routed keys are discarded) and the driver re-expands the
  * chunk in smaller pieces. */
+/* Hash-partitioned isolated FINDORPUT benchmark (configs[1] at N GPUs; the
+ * reference's run_insert_bench, bench.py:120-202, over shards): each shard
+ * runs positions [first, first + count) of one global duplication sequence
+ * (total ops over total / duplication unique keys, generated on the
+ * device), stores the keys owned by peers into their inboxes and
+ * FINDORPUTs its own (gx_shard_bench_route); after a barrier every shard
+ * calls gx_shard_absorb_chunk; gx_shard_bench_result then gives out[0] =
+ * keys INSERTED into this shard, out[1] = TABLE_FULL seen, out[2] =
+ * FINDORPUTs run here, out[3] = keys routed to peers, out[4] = an inbox
+ * overflowed, and *ms = the CUDA-event time of this shard's kernels.  Start
+ * each run with gx_shard_begin(s, 0, 0, &full). */
+int gx_shard_bench_route(gx_shard *s, uint64_t total, uint64_t duplication, uint64_t seed, int32_t key_bits,
+                         uint64_t first, uint64_t count);
+int gx_shard_bench_result(gx_shard *s, uint64_t *out, double *ms);
+
 int gx_shard_set_mode(gx_shard *s, int32_t dedup, int32_t set_log2);
 int gx_shard_set_partitions(gx_shard *s, uint32_t nsub);
 int gx_shard_chunk_status(gx_shard *s, uint64_t *out);

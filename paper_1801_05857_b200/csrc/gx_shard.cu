@@ -27,6 +27,7 @@
 
 #include "gx_level.cuh"
 #include "gx_part.cuh"
+#include "gx_bench.cuh"
 
 namespace gx {
 
@@ -87,6 +88,79 @@ __global__ void __launch_bounds__(256, GX_STAGED_MINB) k_absorb(TableDesc T, Lev
     }
     probes = warp_sum(probes);
     if (lane == 0 && probes) atomicAdd(&A.ctr[LV_PROBES], probes);
+}
+
+// ---- hash-partitioned FINDORPUT benchmark (multi-GPU configs[1]) ---------
+// Positions [first, first + count) of the global duplication sequence
+// (gx_bench.cuh): each warp generates QCAP keys, stores those owned by peers
+// into their inboxes (route_remote, as the level kernel) and FINDORPUTs its
+// own; the peers absorb their inboxes after the barrier (k_absorb).
+// INSERTED results are counted through LevelArgs (out_limit 0: nothing is
+// appended, LV_NEW counts).
+template <int BW, int V>
+__global__ void __launch_bounds__(256, GX_STAGED_MINB) k_bench_routed(TableDesc T, LevelArgs A, RouteArgs R,
+                                                                      BenchArgs B, uint64_t first,
+                                                                      uint64_t count) {
+    using L = StagedSmem<BW, V>;
+    using S = Staged<BW, V>;
+    constexpr int QCAP = QWORDS / V;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * QWORDS;
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::KB;
+    uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    unsigned long long* ovf = R.inbox_ctr[R.rank] + GX_PART_SUB_MAX;
+    unsigned long long probes = 0, routed = 0;
+    const uint64_t end = first + count;
+    for (uint64_t base = first + warp * QCAP; base < end; base += nwarps * QCAP) {
+        const uint32_t m = (uint32_t)min((uint64_t)QCAP, end - base);
+        for (uint32_t k = lane; k < m; k += 32) {
+            uint32_t key[V];
+            bench_key<V>(B, base + k, key);
+#pragma unroll
+            for (int w = 0; w < V; w++) q[k * V + w] = key[w];
+        }
+        __syncwarp();
+        const uint32_t mloc = route_remote<V>(T, R, q, m, ovf, &routed, reinterpret_cast<uint32_t*>(stage));
+        probes += lane == 0 ? mloc : 0;
+        uint32_t full = 0;
+        const uint32_t n_out = probe_staged<BW, V>(T, q, mloc, stage, sbkt, &full);
+        if (__any_sync(FULLMASK, full != 0u) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
+        if (n_out) flush_out<V>(A, q, n_out);
+        __syncwarp();
+    }
+    probes = warp_sum(probes);
+    routed = warp_sum(routed);
+    __threadfence_system();
+    if (lane == 0) {
+        if (probes) atomicAdd(&A.ctr[LV_PROBES], probes);
+        if (routed) atomicAdd(&A.ctr[LV_ROUTED], routed);
+    }
+}
+
+typedef void (*bench_routed_t)(TableDesc, LevelArgs, RouteArgs, BenchArgs, uint64_t, uint64_t);
+
+template <int BW>
+static bench_routed_t pick_bench_routed_v(int v) {
+    switch (v) {
+        case 1: return k_bench_routed<BW, 1>;
+        case 2: return k_bench_routed<BW, 2>;
+        case 4: return k_bench_routed<BW, 4>;
+    }
+    return nullptr;
+}
+
+static bench_routed_t pick_bench_routed(const TableDesc& T) {
+    switch (T.bw) {
+        case 4: return pick_bench_routed_v<4>((int)T.vlen);
+        case 8: return pick_bench_routed_v<8>((int)T.vlen);
+        case 16: return pick_bench_routed_v<16>((int)T.vlen);
+        case 32: return pick_bench_routed_v<32>((int)T.vlen);
+    }
+    return nullptr;
 }
 
 // ---- partitioned dedup mode (gx_part.cuh) ----------------------------
@@ -618,6 +692,72 @@ int gx_shard_expand(gx_shard* s) { return gx_shard_expand_range(s, 0, ~0ull); }
 
 int gx_shard_frontier(const gx_shard* s, uint64_t* n) {
     *n = s->nF;
+    return GX_OK;
+}
+
+int gx_shard_bench_route(gx_shard* s, uint64_t total, uint64_t dup, uint64_t seed, int32_t key_bits,
+                         uint64_t first, uint64_t count) {
+    gx_table* t = s->t;
+    const TableDesc& T = t->d;
+    if (total == 0 || dup == 0 || dup > total || key_bits < 1 || key_bits > 31 || first + count > total) {
+        set_error("bad benchmark parameters (mark-bit tables store at most 31 key bits per word)");
+        return GX_EINPUT;
+    }
+    bench_routed_t k = pick_bench_routed(T);
+    if (!k) {
+        set_error("no routed benchmark kernel for bw=%u vlen=%u", T.bw, T.vlen);
+        return GX_EINPUT;
+    }
+    if (!s->connected) {
+        set_error("shard not connected to its peers");
+        return GX_EINPUT;
+    }
+    if (!s->level_open) level_args(s);
+    s->A.out_limit = 0;  // count INSERTED (LV_NEW), append nothing
+    s->A.cache_mask = 0;
+    BenchArgs B;
+    B.total = total;
+    B.dup = dup;
+    B.unique = total / dup;
+    B.row_base = 0;
+    B.seed = seed;
+    B.key_bits = key_bits;
+    int pb = 1;
+    while ((1ull << pb) < total) pb++;
+    B.perm_bits_n = pb;
+    B.ctr = nullptr;
+    GX_CUDA(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->K.fixed_smem));
+    cudaEvent_t a0 = next_event(s), a1 = next_event(s);
+    GX_CUDA(cudaEventRecord(a0, s->stream));
+    if (count) {
+        k<<<sm_count() * GX_STAGED_MINB, 256, s->K.fixed_smem, s->stream>>>(T, s->A, s->R, B, first, count);
+        GX_LAUNCHED();
+    }
+    GX_CUDA(cudaEventRecord(a1, s->stream));
+    return GX_OK;
+}
+
+int gx_shard_bench_result(gx_shard* s, uint64_t* out, double* ms) {
+    gx_table* t = s->t;
+    unsigned long long* hc = (unsigned long long*)t->h_ctr;
+    uint64_t ovf = 0;
+    GX_CUDA(cudaMemcpyAsync(&ovf, (char*)s->inbox_block + 8 * GX_PART_SUB_MAX, 8, cudaMemcpyDeviceToHost, s->stream));
+    GX_CUDA(cudaMemcpyAsync(hc, t->d_ctr, sizeof(uint64_t) * CTR_N, cudaMemcpyDeviceToHost, s->stream));
+    GX_CUDA(cudaStreamSynchronize(s->stream));
+    double tot = 0;
+    for (size_t i = 0; i + 1 < s->ev_used; i += 2) {
+        float x = 0;
+        GX_CUDA(cudaEventElapsedTime(&x, s->ev[i], s->ev[i + 1]));
+        tot += x;
+    }
+    s->ev_used = 0;
+    s->level_open = false;
+    out[0] = hc[LV_NEW];     // INSERTED (fresh keys stored in this shard)
+    out[1] = hc[LV_FULL];    // TABLE_FULL seen
+    out[2] = hc[LV_PROBES];  // FINDORPUTs run on this shard
+    out[3] = hc[LV_ROUTED];  // keys sent to peers
+    out[4] = ovf;            // an inbox overflowed
+    if (ms) *ms = tot;
     return GX_OK;
 }
 

@@ -61,6 +61,8 @@ class ShardResult:
     levels: int
     digest: tuple | None = None  # reachable-set digest over all ranks (gx_table_digest)
     routed: int = 0  # successors routed to another shard's inbox (all ranks)
+    level_ms: float = 0.0  # CUDA-event time of the level kernels, max over ranks
+    probes: int = 0  # FINDORPUTs issued (all ranks)
 
 
 class DeviceShard:
@@ -249,6 +251,21 @@ class FusedShard:
     def absorb_chunk(self):
         from ._lib import check, lib
         check(lib().gx_shard_absorb_chunk(self._h))
+
+    def bench_route(self, total: int, duplication: int, seed: int, first: int, count: int,
+                    key_bits: int = 31):
+        """Hash-partitioned FINDORPUT benchmark, this shard's positions
+        [first, first + count) of the global sequence (gx_shard_bench_route)."""
+        from ._lib import check, lib
+        check(lib().gx_shard_bench_route(self._h, total, duplication, seed, key_bits, first, count))
+
+    def bench_result(self):
+        """(inserted, table_full, findorputs, routed, overflow), kernel ms"""
+        from ._lib import check, lib, ptr
+        out = np.zeros(5, np.uint64)
+        ms = C.c_double()
+        check(lib().gx_shard_bench_result(self._h, ptr(out, C.c_uint64), C.byref(ms)))
+        return out, ms.value
 
     def set_partitions(self, nsub: int):
         from ._lib import check, lib
@@ -570,9 +587,10 @@ def explore_fused(shards, dist, torch, detect: bool, max_iterations=None,
         dist.all_reduce(t, op=op or dist.ReduceOp.SUM)
         return t.cpu().numpy().astype(np.uint64)
 
-    tot, kept, rounds, outcome, _, routed = _run_levels(list(shards), barrier, reduce, detect, max_iterations,
-                                                        reduce_max=lambda a: reduce(a, dist.ReduceOp.MAX))
+    tot, kept, rounds, outcome, lms, routed = _run_levels(list(shards), barrier, reduce, detect, max_iterations,
+                                                          reduce_max=lambda a: reduce(a, dist.ReduceOp.MAX))
     tot = reduce(tot)
+    lms = float(reduce(np.array([int(lms * 1e6)], np.uint64), dist.ReduceOp.MAX)[0]) / 1e6
     gathered = [None] * dist.get_world_size()
     mine = [s.digest() for s in shards] if digest else []
     dist.all_gather_object(gathered, (kept, mine))
@@ -580,7 +598,8 @@ def explore_fused(shards, dist, torch, detect: bool, max_iterations=None,
     dig = combine_digests(d for _, ds in gathered for d in ds) if digest else None
     return ShardResult(states=int(tot[0]), transitions=int(tot[1]), deadlocks=dls,
                        deadlocks_total=int(tot[3]), expanded=int(tot[2]), iterations=rounds,
-                       outcome=outcome, levels=rounds - 1, digest=dig, routed=routed)
+                       outcome=outcome, levels=rounds - 1, digest=dig, routed=routed, level_ms=lms,
+                       probes=int(tot[4]))
 
 
 def connect_fused(shards, dist):
@@ -670,20 +689,60 @@ def explore_sharded(backend, dist, torch, scheme, initial_packed: np.ndarray, de
                        outcome=outcome, levels=rounds - 1)
 
 
-def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, clock_sampler=None):
+def hash_bench_shards(shards, barrier, reduce, reduce_max, total: int, duplication: int, seed: int = 11):
+    """One run of the hash-partitioned FINDORPUT benchmark over `shards`
+    (this process's; the peers' run in theirs): the global sequence of
+    `total` ops is split evenly over all shards, each routes the keys it
+    does not own, then every shard absorbs.  Returns the global
+    (inserted, found, table_full, max kernel ms over shards and ranks)."""
+    from ctypes import c_int32
+    from ._lib import check, lib
+    world = shards[0].world
+    for s in shards:
+        full = c_int32()
+        check(lib().gx_shard_begin(s.handle, 0, 0, C.byref(full)))
+    for s in shards:
+        per = total // world
+        first = s.rank * per
+        count = per if s.rank < world - 1 else total - first
+        s.bench_route(total, duplication, seed, first, count)
+    barrier()
+    for s in shards:
+        s.absorb_chunk()
+    st = np.zeros(5, np.uint64)
+    ms = 0.0
+    for s in shards:
+        o, m = s.bench_result()
+        st += o
+        ms = max(ms, m)
+    st = reduce(st)
+    ms = float(reduce_max(np.array([int(ms * 1e6)], np.uint64))[0]) / 1e6
+    if st[4]:
+        raise RuntimeError("inbox overflow in the sharded hash benchmark; raise inbox_capacity")
+    inserted = int(st[0])
+    return {"ops": total, "duplication": duplication, "inserted": inserted, "found": total - inserted,
+            "table_full": bool(st[1]), "routed": int(st[3]), "ms": ms,
+            "ops_per_sec": total / (ms / 1e3) if ms > 0 else 0.0}
+
+
+def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, clock_sampler=None,
+                  cpu_fn=None, peaks=None, golden=None):
     """bench.py's N > 1 leg: one model hash-partitioned over N GPUs (strong
     scaling), fused peer-routed levels.  Device time = CUDA events around
     the K timed explorations, max over ranks; e2e = the same through
-    shard construction (CSR upload, table + inbox allocation, IPC mapping)
-    per step."""
-    import json as _json
+    shard construction (CSR upload from host memory, table + inbox
+    allocation, IPC mapping) per step.  Also the hash-partitioned isolated
+    FINDORPUT benchmark (configs[1] at N GPUs, weak scaling: 2^28 ops per
+    GPU), the roofline of the level kernels, the reachable-set digest
+    against the golden one, and (rank 0) the CPU reference sample."""
     import tempfile
     import time
     from pathlib import Path
 
     from . import _lib, statevec
-    from .explore import ExploreConfig
+    from .explore import DeviceNetwork, ExploreConfig
     from .hashtable import TableConfig
+
     from .network import load_network
 
     rank, world = dist.get_rank(), dist.get_world_size()
@@ -703,7 +762,7 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, cl
     cfg = ExploreConfig(table=TableConfig(bucket_words=args.bucket_words,
                                           num_hash_functions=args.hash_functions,
                                           capacity_words=cap_words), detect_deadlocks=True,
-                        cache_slots=max(1, args.cache_slots))
+                        cache_slots=max(1, args.cache_slots), dedup=getattr(args, "dedup", False))
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream().cuda_stream
     # frontier: two adjacent levels with margin; inbox: most of what is left
@@ -731,17 +790,19 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, cl
     shard = make()
     res = None
     for _ in range(args.warmup):
-        res = explore_fused(shard, dist, torch, True, device=dev)
+        res = explore_fused(shard, dist, torch, True, device=dev, digest=False)
     torch.cuda.synchronize()
     dist.barrier()
     l0 = _lib.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ctx = clock_sampler if clock_sampler is not None else _Null()
+    lms = []
     with ctx:
         torch.cuda.synchronize()
         e0.record()
         for _ in range(args.steps):
-            res = explore_fused(shard, dist, torch, True, device=dev)
+            res = explore_fused(shard, dist, torch, True, device=dev, digest=False)
+            lms.append(res.level_ms)
         e1.record()
         torch.cuda.synchronize()
     dist.barrier()
@@ -749,15 +810,22 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, cl
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
+    # set identity of the last timed run (all shards' tables still hold it)
+    mine = [s.digest() for s in shard]
+    parts = [None] * world
+    dist.all_gather_object(parts, mine)
+    digest = list(combine_digests(d for p in parts for d in p))
     close(shard)
     assert (res.states, res.transitions) == cf, (res.states, res.transitions, cf)
+    if golden and golden.get("digest"):
+        assert digest == golden["digest"], (digest, golden["digest"])
     # e2e: shards built (CSR from host memory, tables, inboxes, IPC) every step
     e2e = []
     for i in range(args.e2e_steps + 1):
         dist.barrier()
         t0 = time.perf_counter()
         sh = make()
-        r = explore_fused(sh, dist, torch, True, device=dev)
+        r = explore_fused(sh, dist, torch, True, device=dev, digest=False)
         close(sh)
         torch.cuda.synchronize()
         t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
@@ -765,6 +833,59 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, cl
         if i:
             e2e.append(float(t.item()))
     e2e_value = r.states * len(e2e) / sum(e2e) if e2e else None
+    dn = DeviceNetwork(net, scheme)
+    csr_bytes = (dn.csr_bytes + 4 * vlen) * gworld
+    dn.close()
+
+    # roofline of the level kernels (all GPUs): SURVEY §8(d) bytes, plus the
+    # probe-based bytes and the NVLink bytes of the routed successors
+    hbm = (peaks or {}).get("hbm_gbs", 6650.0)
+    sbw = max(32, 4 * args.bucket_words)
+    level_ms = sum(lms) / len(lms)
+    alg = res.transitions * sbw + res.states * 12 * vlen
+    probe_b = res.probes * sbw + res.states * 12 * vlen + res.routed * 8 * vlen
+    achieved = alg / (level_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm * world, "unit": "GB/s",
+            "frac": achieved / (hbm * world), "traffic": None,
+            "kernel": "k_level_routed + k_absorb (all GPUs)", "algorithmic_bytes_per_step": alg,
+            "kernel_ms_per_step": level_ms, "bytes_model": "transitions*max(32,4*bw) + states*12*vlen",
+            "probe_bytes_per_step": probe_b,
+            "frac_probe_based": probe_b / (level_ms / 1e3) / 1e9 / (hbm * world),
+            "nvlink_bytes_per_step": res.routed * 4 * vlen,
+            "peak_note": f"{hbm} GB/s per GPU (MEASURED_PEAKS.json) x {world}"}
+
+    # the hash-partitioned FINDORPUT benchmark: 2^28 ops per GPU, 2-word keys
+    hash_rows = []
+    if not getattr(args, "no_hash_bench", False):
+        ops = (1 << 28) * world
+        for d in (1, 10):
+            per = (ops // d) // gworld + ((ops // d) >> 6) // gworld + 4096
+            hcfg = ExploreConfig(table=TableConfig(bucket_words=32, num_hash_functions=8,
+                                                   capacity_words=table_capacity(per, 2, 32, 0.5)))
+            # any network with 2-word states and a spare top bit gives the
+            # table geometry (keys are 31-bit words): the token ring N=19
+            hnet = load_network(model_path("ring19", tmp))
+            hs = [FusedShard(hnet, hcfg, rank * local + l, gworld, inbox_capacity=ops // gworld + (1 << 20),
+                             frontier_capacity=1 << 16, stream=stream, status=False) for l in range(local)]
+            connect_fused(hs, dist)
+
+            def barrier():
+                dist.barrier()
+
+            def red(a, op=None):
+                t = torch.from_numpy(a.astype(np.int64)).to(dev)
+                dist.all_reduce(t, op=op or dist.ReduceOp.SUM)
+                return t.cpu().numpy().astype(np.uint64)
+
+            hash_bench_shards(hs, barrier, red, lambda a: red(a, dist.ReduceOp.MAX), ops, d)  # warm-up
+            row = hash_bench_shards(hs, barrier, red, lambda a: red(a, dist.ReduceOp.MAX), ops, d)
+            for h in hs:
+                h.close()
+            assert row["inserted"] == ops // d and not row["table_full"], row
+            row.update({"bw": 32, "vlen": 2, "n_gpus": world, "ops_per_gpu": ops // world,
+                        "gbs_alg": ops * sbw / (row["ms"] / 1e3) / 1e9})
+            hash_rows.append(row)
+    cpu = cpu_fn() if (cpu_fn is not None and rank == 0) else None
     return {
         "metric": "states explored/sec", "value": res.states * args.steps / (ms / 1e3),
         "unit": "states/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -781,10 +902,14 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, cl
                                   "routed to the owner's inbox by P2P stores inside the level "
                                   "kernel (CUDA IPC over NVLink), NCCL all_reduce of level "
                                   "counters"},
-        "roofline": None, "cpu_baseline": None,
-        "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": None,
-                "d2h_bytes_per_step": None,
+        "roofline": roof, "cpu_baseline": cpu,
+        "digest": {"value": digest, "golden": (golden or {}).get("digest"),
+                   "equal": digest == (golden or {}).get("digest")},
+        "e2e": {"value": e2e_value, "unit": "states/s", "h2d_bytes_per_step": csr_bytes,
+                "d2h_bytes_per_step": (res.levels + 2) * 64 * gworld + 400 * vlen,
                 "api": "FusedShard + connect_fused + explore_fused per step"},
+        "hash_bench_sharded": hash_rows,
+        "routed_per_step": res.routed, "probes_per_step": res.probes,
         "gpu_launches": launches,
         "clocks": clock_sampler.summary() if clock_sampler is not None else None,
     }
