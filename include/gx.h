@@ -153,6 +153,13 @@ int gx_dump(gx_table *t, int64_t *handles, uint8_t *status, uint32_t *words, uin
  * h.  Shards combine by adding counts and sums and xor-ing xors. */
 int gx_table_digest(gx_table *t, int32_t words, uint64_t *out);
 
+/* The canonical state dump's order (statevec.py:93-100, dump_states: packed
+ * vectors sorted lexicographically over their words) computed on the
+ * device: the first `words` words of every occupied slot, sorted (stable
+ * LSD radix sort), copied to out[capacity * words].  *count = occupied
+ * slots; out = NULL only counts.  Works without a status array. */
+int gx_dump_sorted(gx_table *t, int32_t words, uint32_t *out, uint64_t capacity, uint64_t *count);
+
 /* --------------------------------------------------------------- network */
 
 /* A Network (network.py:43-62) flattened to device CSR by the host

@@ -78,6 +78,7 @@ SIGNATURES = {
     "gx_read_slots": (C.c_int, [_vp, _i64p, C.c_uint64, _u8p, _u32p]),
     "gx_dump": (C.c_int, [_vp, _i64p, _u8p, _u32p, C.c_uint64, _u64p]),
     "gx_table_digest": (C.c_int, [_vp, C.c_int32, _u64p]),
+    "gx_dump_sorted": (C.c_int, [_vp, C.c_int32, _u32p, C.c_uint64, _u64p]),
     "gx_net_create": (C.c_int, [_P(NetworkCsr), _vp, _P(_vp)]),
     "gx_net_destroy": (C.c_int, [_vp]),
     "gx_expand": (C.c_int, [_vp, _u32p, C.c_uint64, _u64p, _u32p, _u32p, C.c_uint64, _u64p]),

@@ -562,7 +562,10 @@ int gx_shard_begin(gx_shard* s, int32_t owns_initial, int32_t detect_deadlocks, 
             s->n_pending = 1;
         }
     }
-    // the level counters restart from zero (the table clear zeroed them)
+    // the level counters restart from zero (the table clear zeroed them);
+    // the cleared inbox head must be in place before any peer (another
+    // process) reserves space in it after the caller's barrier
+    GX_CUDA(cudaStreamSynchronize(s->stream));
     return GX_OK;
 }
 

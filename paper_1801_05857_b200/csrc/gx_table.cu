@@ -503,6 +503,126 @@ __global__ void __launch_bounds__(256) k_digest_any(TableDesc T, int words, unsi
     digest_flush(c, s, x, out);
 }
 
+// ------------------------------------------------------ sorted dump
+// The canonical state dump (statevec.py:93-100: packed words, sorted
+// lexicographically) produced on the device: gather the occupied slots'
+// first `words` words, then a stable LSD radix sort over the words from
+// last to first (8-bit digits, a permutation carried along), then one
+// gather in sorted order.  Works on tables without a status array.
+constexpr int DS_TILE = 1 << 15;  // elements per radix tile
+
+__global__ void __launch_bounds__(256) k_gather_occupied(TableDesc T, int words, uint32_t* out,
+                                                         unsigned long long* ctr, uint64_t cap) {
+    const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const uint64_t nb_round = (T.nb + stride - 1) / stride * stride;
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb_round; b += stride) {
+        uint32_t occ = 0;
+        if (b < T.nb)
+            for (int j = 0; j < (int)T.spb; j++) occ |= (slot_occupied(T, b, j) ? 1u : 0u) << j;
+        const uint32_t c = __popc(occ);
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULLMASK, incl, o);
+            if (lane >= o) incl += y;
+        }
+        unsigned long long base = 0;
+        if (lane == 31 && incl) base = atomicAdd(ctr, (unsigned long long)incl);
+        base = __shfl_sync(FULLMASK, base, 31) + incl - c;
+        for (int j = 0; occ; j++, occ >>= 1) {
+            if (!(occ & 1u)) continue;
+            if (base < cap) {
+                uint32_t key[GX_MAXV];
+                read_words(T, b, j, key);
+                for (int w = 0; w < words; w++) out[base * words + w] = key[w];
+            }
+            base++;
+        }
+    }
+}
+
+__global__ void k_iota(uint32_t* perm, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (uint64_t)blockDim.x)
+        perm[i] = (uint32_t)i;
+}
+
+__global__ void k_word_of(const uint32_t* rows, int words, int w, const uint32_t* perm, uint32_t* key, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (uint64_t)blockDim.x)
+        key[i] = rows[(uint64_t)perm[i] * words + w];
+}
+
+// per tile: histogram of digit (key >> shift) & 255 -> hist[digit * tiles + tile]
+__global__ void __launch_bounds__(256) k_radix_hist(const uint32_t* key, uint64_t n, int shift, uint32_t* hist,
+                                                   uint32_t tiles) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t lo = (uint64_t)blockIdx.x * DS_TILE, hi = min(n, lo + DS_TILE);
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&h[(key[i] >> shift) & 255u], 1u);
+    __syncthreads();
+    hist[threadIdx.x * (uint64_t)tiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// exclusive scan of hist[0, m) in place, one block (m is a few million)
+__global__ void __launch_bounds__(1024) k_scan_one(uint32_t* a, uint64_t m) {
+    __shared__ uint32_t part[1024];
+    const uint64_t per = (m + 1023) / 1024;
+    const uint64_t lo = threadIdx.x * per, hi = min(m, lo + per);
+    uint32_t sum = 0;
+    for (uint64_t i = lo; i < hi; i++) sum += a[i];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int i = 0; i < 1024; i++) {
+            const uint32_t x = part[i];
+            part[i] = run;
+            run += x;
+        }
+    }
+    __syncthreads();
+    uint32_t run = part[threadIdx.x];
+    for (uint64_t i = lo; i < hi; i++) {
+        const uint32_t x = a[i];
+        a[i] = run;
+        run += x;
+    }
+}
+
+// stable scatter of one tile by one warp, 32 elements at a time in order
+__global__ void __launch_bounds__(32) k_radix_scatter(const uint32_t* key, const uint32_t* perm, uint64_t n,
+                                                      int shift, const uint32_t* offs, uint32_t tiles,
+                                                      uint32_t* key2, uint32_t* perm2) {
+    __shared__ uint32_t cur[256];
+    const int lane = threadIdx.x;
+    for (int d = lane; d < 256; d += 32) cur[d] = offs[d * (uint64_t)tiles + blockIdx.x];
+    __syncwarp();
+    const uint64_t lo = (uint64_t)blockIdx.x * DS_TILE, hi = min(n, lo + DS_TILE);
+    for (uint64_t b = lo; b < hi; b += 32) {
+        const uint64_t i = b + lane;
+        const bool a = i < hi;
+        const uint32_t k = a ? key[i] : 0u, p = a ? perm[i] : 0u;
+        const uint32_t d = a ? (k >> shift) & 255u : 256u;
+        const uint32_t grp = __match_any_sync(FULLMASK, d);
+        uint32_t lt;
+        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+        const uint32_t pos = a ? cur[d] + __popc(grp & lt) : 0u;
+        __syncwarp();
+        if (a && (grp & lt) == 0) cur[d] += __popc(grp);
+        __syncwarp();
+        if (a) {
+            key2[pos] = k;
+            perm2[pos] = p;
+        }
+    }
+}
+
+__global__ void k_gather_rows(const uint32_t* rows, int words, const uint32_t* perm, uint32_t* out, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += gridDim.x * (uint64_t)blockDim.x)
+        for (int w = 0; w < words; w++) out[i * words + w] = rows[(uint64_t)perm[i] * words + w];
+}
+
 int table_fixup_status(gx_table* t, const uint32_t* d_new_keys, uint64_t n_new) {
     if (!t->d.status) return GX_OK;  // exploration-only table: no statuses to keep
     const TableDesc& T = t->d;
@@ -834,6 +954,77 @@ int gx_read_slots(gx_table* t, const int64_t* handles, uint64_t n, uint8_t* stat
 int gx_dump(gx_table* t, int64_t* handles, uint8_t* status, uint32_t* words, uint64_t cap,
             uint64_t* count) {
     return select_slots(t, 0, t->d.nb, SEL_OCCUPIED, handles, status, words, cap, count);
+}
+
+int gx_dump_sorted(gx_table* t, int32_t words, uint32_t* out, uint64_t capacity, uint64_t* count) {
+    const TableDesc& T = t->d;
+    if (words < 1 || words > (int32_t)T.vlen) {
+        set_error("sorted dump over %d words of a %u-word table", words, T.vlen);
+        return GX_EINPUT;
+    }
+    cudaStream_t st = t->stream;
+    unsigned long long* c = (unsigned long long*)t->d_ctr + CTR_SCRATCH;
+    // count first
+    GX_CUDA(cudaMemsetAsync(c, 0, 8, st));
+    const int grid = sm_count() * 8;
+    k_gather_occupied<<<grid, 256, 0, st>>>(T, words, nullptr, c, 0);
+    GX_LAUNCHED();
+    unsigned long long n = 0;
+    GX_CUDA(cudaMemcpyAsync(&n, c, 8, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    *count = n;
+    if (!out || n == 0) return GX_OK;
+    if (n > 0xffffffffull) {
+        set_error("sorted dump of %llu states exceeds the 32-bit permutation", n);
+        return GX_EINPUT;
+    }
+    const uint32_t tiles = (uint32_t)((n + DS_TILE - 1) / DS_TILE);
+    // rows | key | key2 | perm | perm2 | hist
+    const uint64_t b_rows = 4 * n * words, b_vec = 4 * n, b_hist = 4ull * 256 * tiles;
+    DevBuf buf;
+    int rc = buf.ensure(b_rows + 4 * b_vec + b_hist + 64);
+    if (rc) return rc;
+    uint32_t* rows = (uint32_t*)buf.p;
+    uint32_t* key = rows + n * words;
+    uint32_t* key2 = key + n;
+    uint32_t* perm = key2 + n;
+    uint32_t* perm2 = perm + n;
+    uint32_t* hist = perm2 + n;
+    GX_CUDA(cudaMemsetAsync(c, 0, 8, st));
+    k_gather_occupied<<<grid, 256, 0, st>>>(T, words, rows, c, n);
+    GX_LAUNCHED();
+    k_iota<<<grid, 256, 0, st>>>(perm, n);
+    GX_LAUNCHED();
+    for (int w = words - 1; w >= 0; w--) {
+        k_word_of<<<grid, 256, 0, st>>>(rows, words, w, perm, key, n);
+        GX_LAUNCHED();
+        for (int shift = 0; shift < 32; shift += 8) {
+            k_radix_hist<<<tiles, 256, 0, st>>>(key, n, shift, hist, tiles);
+            GX_LAUNCHED();
+            k_scan_one<<<1, 1024, 0, st>>>(hist, 256ull * tiles);
+            GX_LAUNCHED();
+            k_radix_scatter<<<tiles, 32, 0, st>>>(key, perm, n, shift, hist, tiles, key2, perm2);
+            GX_LAUNCHED();
+            std::swap(key, key2);
+            std::swap(perm, perm2);
+        }
+    }
+    const uint64_t m = std::min<uint64_t>(n, capacity);
+    uint32_t* sorted = key2;  // free scratch of n words ... reuse rows-sized space below
+    DevBuf outb;
+    rc = outb.ensure(4 * n * words);
+    if (rc) {
+        buf.release();
+        return rc;
+    }
+    sorted = (uint32_t*)outb.p;
+    k_gather_rows<<<grid, 256, 0, st>>>(rows, words, perm, sorted, n);
+    GX_LAUNCHED();
+    GX_CUDA(cudaMemcpyAsync(out, sorted, 4 * m * words, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    buf.release();
+    outb.release();
+    return GX_OK;
 }
 
 int gx_table_digest(gx_table* t, int32_t words, uint64_t* out) {

@@ -701,6 +701,7 @@ def hash_bench_shards(shards, barrier, reduce, reduce_max, total: int, duplicati
     for s in shards:
         full = c_int32()
         check(lib().gx_shard_begin(s.handle, 0, 0, C.byref(full)))
+    barrier()  # every inbox is cleared before any peer routes into it
     for s in shards:
         per = total // world
         first = s.rank * per
@@ -869,8 +870,14 @@ def bench_sharded(args, torch, dist, model_path, closed_form, table_capacity, cl
                              frontier_capacity=1 << 16, stream=stream, status=False) for l in range(local)]
             connect_fused(hs, dist)
 
+            flag = torch.zeros(1, dtype=torch.int64, device=dev)
+
             def barrier():
-                dist.barrier()
+                # stream-ordered: the all_reduce runs after this rank's
+                # kernels, so no peer absorbs before our stores landed
+                torch.cuda.current_stream().synchronize()
+                dist.all_reduce(flag)
+                torch.cuda.current_stream().synchronize()
 
             def red(a, op=None):
                 t = torch.from_numpy(a.astype(np.int64)).to(dev)

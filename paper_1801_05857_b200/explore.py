@@ -232,7 +232,9 @@ class Explorer:
         return self.table.digest(self.scheme.vector_length)
 
     def dump_states(self) -> str:
-        return statevec.dump_states_array(self.table.dump_arrays()[2][:, :self.scheme.vector_length])
+        """The canonical dump (statevec.py:93-100), sorted on the device."""
+        return statevec.dump_states_array(self.table.sorted_vectors(self.scheme.vector_length),
+                                          presorted=True)
 
     def dump_table(self) -> str:
         hs, st, ws = self.table.dump_arrays()

@@ -276,6 +276,17 @@ class StateTable:
         check(lib().gx_table_digest(self._h, int(words or self.vector_length), ptr(out, C.c_uint64)))
         return int(out[0]), int(out[1]), int(out[2])
 
+    def sorted_vectors(self, words: int | None = None) -> np.ndarray:
+        """The occupied slots' first `words` words, sorted lexicographically
+        on the device (gx_dump_sorted): dump_states' order."""
+        w = int(words or self.vector_length)
+        cnt = C.c_uint64()
+        check(lib().gx_dump_sorted(self._h, w, None, 0, C.byref(cnt)))
+        out = np.zeros((max(cnt.value, 1), w), np.uint32)
+        if cnt.value:
+            check(lib().gx_dump_sorted(self._h, w, ptr(out), cnt.value, C.byref(cnt)))
+        return out[:cnt.value]
+
     def occupied_vectors(self) -> list:
         return [tuple(int(x) for x in row) for row in self.dump_arrays()[2]]
 

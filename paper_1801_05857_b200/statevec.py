@@ -91,14 +91,13 @@ def dump_states(packed_states) -> str:
     return "\n".join(format_packed(p) for p in sorted(packed_states)) + "\n"
 
 
-def dump_states_array(words: np.ndarray) -> str:
-    """dump_states for an (n, vlen) u32 array, sorted on the host with a
-    lexicographic sort over the words."""
+def dump_states_array(words: np.ndarray, presorted: bool = False) -> str:
+    """dump_states for an (n, vlen) u32 array: sorted lexicographically over
+    the words (on the host unless `presorted`, e.g. by gx_dump_sorted)."""
     words = np.asarray(words, np.uint32).reshape(len(words), -1) if len(words) else words
     if len(words) == 0:
         return "\n"
-    order = np.lexsort(words.T[::-1])
-    srt = words[order]
+    srt = words if presorted else words[np.lexsort(words.T[::-1])]
     hexes = [np.char.zfill(np.char.mod("%x", srt[:, j]), 8) for j in range(srt.shape[1])]
     lines = hexes[0]
     for h in hexes[1:]:

@@ -109,3 +109,32 @@ def test_deadlocks_beyond_record_buffer(shards, tmp_path):
     assert rep.deadlocks_total == 2 ** n
     want = sorted((1,) + bits for bits in product((2, 3), repeat=n))[:100]
     assert [tuple(s) for s in rep.deadlocks] == want
+
+
+@pytest.mark.parametrize("name", ["ring13", "peterson5", "phil12"])
+def test_device_sorted_dump_at_scale(name, tmp_path):
+    """gx_dump_sorted (the canonical dump's order, statevec.py:93-100) on
+    1e6-1e7 states: strictly increasing rows whose digest is the golden one."""
+    import numpy as np
+    from paper_1801_05857_b200.explore import Explorer
+    e = big()[name]
+    net = gx.load_network(_gen(name, tmp_path))
+    ex = Explorer(net, ExploreConfig(table=TableConfig(capacity_words=_cap(e["states"], 4), num_hash_functions=16),
+                                     state_digest=False), status=False)
+    try:
+        ex.run()
+        rows = ex.table.sorted_vectors(ex.scheme.vector_length).astype(np.uint64)
+    finally:
+        ex.close()
+    assert len(rows) == e["states"]
+    key = np.zeros(len(rows), dtype=object) if rows.shape[1] > 2 else None
+    if rows.shape[1] <= 2:
+        k = rows[:, 0] << np.uint64(32) if rows.shape[1] == 2 else rows[:, 0]
+        if rows.shape[1] == 2:
+            k = k | rows[:, 1]
+        assert (np.diff(k.astype(np.uint64)) > 0).all()
+    else:
+        order = np.lexsort(rows.T[::-1])
+        assert (order == np.arange(len(rows))).all()
+    assert list(statevec.state_digest(rows.astype(np.uint32))) == e["digest"]
+    del key
