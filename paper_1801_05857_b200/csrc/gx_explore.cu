@@ -578,9 +578,10 @@ __global__ void __launch_bounds__(256, 2) k_bench_staged(TableDesc T, BenchArgs 
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * (KB * V);
-    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + 8ull * KB * V * 4) + wid * KB;
-    uint4* stage = reinterpret_cast<uint4*>(smem + 8ull * KB * V * 4 + 8ull * KB * 8 +
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + 8ull * KB * V * 4) + wid * S::SB_STRIDE;
+    uint4* stage = reinterpret_cast<uint4*>(smem + 8ull * KB * V * 4 + 8ull * S::SB_STRIDE * 8 +
                                             (size_t)wid * S::STAGE_BYTES);
+    staged_init(sbkt, KB);
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
     unsigned long long ins = 0, full = 0, loads = 0;
@@ -613,7 +614,7 @@ __global__ void __launch_bounds__(256, 2) k_bench_staged(TableDesc T, BenchArgs 
 template <int BW, int V>
 static size_t bench_staged_smem() {
     using S = Staged<BW, V>;
-    return 8ull * S::KB * V * 4 + 8ull * S::KB * 8 + 8ull * S::STAGE_BYTES;
+    return 8ull * S::KB * V * 4 + 8ull * S::SB_STRIDE * 8 + 8ull * S::STAGE_BYTES;
 }
 
 struct BenchKernel {

@@ -298,6 +298,112 @@ __device__ __forceinline__ uint32_t route_remote(const TableDesc& T, const Route
     return self < 0 ? 0u : cur[self];
 }
 
+// Cache filter and owner routing of q[0, m) in two passes instead of
+// three (cache_filter + route_remote): pass 1 computes each key's 32-bit
+// mix once for its cache slot AND its owner, drops cache hits, compacts the
+// kept keys stably to the front of q and counts keys per owner (match_any
+// leaders); then one reservation atomic per (call, remote owner); pass 2
+// stores remote keys to their owner's inbox (consecutive per owner) and
+// compacts own keys again.  Returns the number of own keys; *routed
+// (lane 0) counts keys sent.  scratch: 96 u32 of the warp's idle stage
+// buffer.  Results are those of cache_filter + route_remote.
+template <int V, bool ROUTE>
+__device__ __forceinline__ uint32_t filter_route(const TableDesc& T, const RouteArgs& R, unsigned long long* cache,
+                                                 uint32_t cmask, uint32_t* q, uint32_t m, unsigned long long* ovf,
+                                                 unsigned long long* routed, uint32_t* scratch) {
+    const int lane = threadIdx.x & 31;
+    const int world = ROUTE ? R.world : 1;
+    const int self = ROUTE ? R.rank : 0;
+    uint32_t* cnt = scratch;   // [32] keys per owner
+    uint32_t* cur = scratch + 32;  // [32] owner cursors (pass 2)
+    if (ROUTE) {
+        cnt[lane] = 0;
+        cur[lane] = 0;
+        __syncwarp();
+    }
+    uint32_t kept = 0;
+    for (uint32_t r0 = 0; r0 < m; r0 += 32) {
+        const uint32_t e = r0 + lane;
+        const bool a = e < m;
+        uint32_t key[V];
+#pragma unroll
+        for (int w = 0; w < V; w++) key[w] = a ? q[e * V + w] : 0u;
+        bool keep = a;
+        int o = -1;
+        if (a) {
+            const uint32_t x = key_mix<V>(key);
+            if (cmask) {
+                const unsigned long long kv = cache_word<V>(T, key);
+                keep = atomicExch(&cache[x & cmask], kv) != kv;
+            }
+            if (keep && ROUTE) o = owner_of_mix(x, world);
+        }
+        if (ROUTE) {
+            const uint32_t grp = __match_any_sync(FULLMASK, o);
+            if (o >= 0 && (grp & lanemask_lt()) == 0) cnt[o] += __popc(grp);
+        }
+        const uint32_t km = __ballot_sync(FULLMASK, keep);
+        __syncwarp();
+        if (keep) {
+            const uint32_t p = kept + __popc(km & lanemask_lt());
+#pragma unroll
+            for (int w = 0; w < V; w++) q[p * V + w] = key[w];
+        }
+        kept += __popc(km);
+        __syncwarp();
+    }
+    if (!ROUTE) return kept;
+    // reserve room in every peer inbox at once (independent remote atomics)
+    const uint32_t mine = lane < world ? cnt[lane] : 0u;
+    unsigned long long base = 0;
+    bool ok = true;
+    if (lane < world && lane != self && mine) {
+        base = atomicAdd(R.inbox_ctr[lane], (unsigned long long)mine);
+        if (base + mine > R.inbox_cap) {
+            ok = false;
+            atomicExch(ovf, 1ull);
+        }
+    }
+    const uint32_t sent = __reduce_add_sync(FULLMASK, lane != self ? mine : 0u);
+    if (lane == 0) *routed += sent;
+    // pass 2: scatter (peer stores, consecutive per owner) / compact local
+    for (uint32_t r0 = 0; r0 < kept; r0 += 32) {
+        const uint32_t e = r0 + lane;
+        int o = -1;
+        uint32_t key[V];
+#pragma unroll
+        for (int w = 0; w < V; w++) key[w] = 0u;
+        if (e < kept) {
+#pragma unroll
+            for (int w = 0; w < V; w++) key[w] = q[e * V + w];
+            o = owner_of_mix(key_mix<V>(key), world);
+        }
+        const uint32_t grp = __match_any_sync(FULLMASK, o);
+        const uint32_t pos = (o >= 0 ? cur[o] : 0u) + __popc(grp & lanemask_lt());
+        const int src = o < 0 ? 0 : o;
+        const unsigned long long b_o = __shfl_sync(FULLMASK, base, src);
+        const int ok_o = __shfl_sync(FULLMASK, ok ? 1 : 0, src);
+        __syncwarp();
+        if (o >= 0 && (grp & lanemask_lt()) == 0) cur[o] += __popc(grp);
+        if (o >= 0 && o != self) {
+            if (ok_o) {
+                uint32_t* dst = R.inbox[o] + (b_o + pos) * (uint64_t)V;
+                if (V == 2) {
+                    *reinterpret_cast<uint2*>(dst) = make_uint2(key[0], key[1 % V]);
+                } else {
+#pragma unroll
+                    for (int w = 0; w < V; w++) dst[w] = key[w];
+                }
+            }
+        } else if (o == self) {
+#pragma unroll
+            for (int w = 0; w < V; w++) q[pos * V + w] = key[w];
+        }
+        __syncwarp();
+    }
+    return cur[self];
+}
+
 // The same level with the FINDORPUT of each successor chunk done by
 // probe_staged (gx_staged.cuh): bucket loads staged in shared memory with
 // cp.async, KB buckets in flight per warp.  All per-warp buffers live in
@@ -307,7 +413,7 @@ template <int BW, int V>
 struct StagedSmem {
     using S = Staged<BW, V>;
     static constexpr size_t Q = 8ull * QWORDS * 4;
-    static constexpr size_t B = 8ull * S::KB * 8;
+    static constexpr size_t B = 8ull * S::SB_STRIDE * 8;
     static constexpr size_t ST = 8ull * S::STAGE_BYTES;
     static constexpr size_t FIXED = Q + B + ST;
 };
@@ -322,9 +428,10 @@ __device__ __forceinline__ void level_staged_body(const TableDesc& T, const NetD
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * QWORDS;
-    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::KB;
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::SB_STRIDE;
     uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
     unsigned long long* dcache = reinterpret_cast<unsigned long long*>(smem + L::FIXED);
+    staged_init(sbkt, S::KB);
     const uint32_t cmask = V <= 2 ? A.cache_mask : 0u;
     if (cmask) {
         for (uint32_t i = threadIdx.x; i <= cmask; i += blockDim.x) dcache[i] = 0ull;
@@ -376,11 +483,15 @@ __device__ __forceinline__ void level_staged_body(const TableDesc& T, const NetD
             }
             __syncwarp();
             uint32_t m = c1 - c0;
-            if (cmask) m = cache_filter<V>(T, dcache, cmask, q, m);
-            if (V <= 2 && A.gfilter_mask) m = global_filter<V>(T, A.gfilter, A.gfilter_mask, q, m);
-            if (ROUTE)
-                m = route_remote<V>(T, R, q, m, &A.ctr[LV_OVF], &routed,
-                                    reinterpret_cast<uint32_t*>(stage));  // stage is idle here
+            if (V <= 2 && A.gfilter_mask) {  // the GPU-wide filter (off by default): the separate passes
+                if (cmask) m = cache_filter<V>(T, dcache, cmask, q, m);
+                m = global_filter<V>(T, A.gfilter, A.gfilter_mask, q, m);
+                if (ROUTE)
+                    m = route_remote<V>(T, R, q, m, &A.ctr[LV_OVF], &routed, reinterpret_cast<uint32_t*>(stage));
+            } else if (ROUTE || cmask) {
+                m = filter_route<V, ROUTE>(T, R, dcache, cmask, q, m, &A.ctr[LV_OVF], &routed,
+                                           reinterpret_cast<uint32_t*>(stage));  // stage is idle here
+            }
             probes += lane == 0 ? m : 0;
             uint32_t full = 0;
             const uint32_t n_out = probe_staged<BW, V>(T, q, m, stage, sbkt, &full);

@@ -59,8 +59,9 @@ __global__ void __launch_bounds__(256, GX_STAGED_MINB) k_absorb(TableDesc T, Lev
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * QWORDS;
-    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::KB;
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::SB_STRIDE;
     uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
+    staged_init(sbkt, S::KB);
     unsigned long long* dcache = reinterpret_cast<unsigned long long*>(smem + L::FIXED);
     const uint32_t cmask = V <= 2 ? A.cache_mask : 0u;
     if (cmask) {
@@ -108,8 +109,9 @@ __global__ void __launch_bounds__(256, GX_STAGED_MINB) k_bench_routed(TableDesc 
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * QWORDS;
-    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::KB;
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::SB_STRIDE;
     uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
+    staged_init(sbkt, S::KB);
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
     unsigned long long* ovf = R.inbox_ctr[R.rank] + GX_PART_SUB_MAX;

@@ -34,6 +34,9 @@
 #ifndef GX_STAGE_KB_MAX
 #define GX_STAGE_KB_MAX 32  // keys per staged batch at most (B200 sweeps: 3 blocks x 32 > 2 blocks x 64)
 #endif
+#ifndef GX_TMA
+#define GX_TMA 0  // 1: stage buckets with one bulk copy (TMA) per key instead of BW/4 cp.async (B200: 5-10% slower, profiles/README.md)
+#endif
 
 namespace gx {
 
@@ -122,7 +125,49 @@ struct Staged {
                                                                              : GX_STAGE_BYTES / (4 * BW));
     static constexpr int STAGE_BYTES = KB * 4 * BW;   // per warp
     static constexpr int KPL = KB / 32;               // keys per lane per batch
+    // u64 words per warp of the index array: KB bucket indices, then the
+    // warp's TMA mbarrier and its phase
+    static constexpr int SB_STRIDE = KB + 2;
 };
+
+// ---------------------------------------------------- TMA bucket staging
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// once per warp before its first probe_staged: the warp's mbarrier (one
+// arrival per round: lane 0's expect_tx) and its phase bit
+__device__ __forceinline__ void staged_init(unsigned long long* sbkt, int kb) {
+#if GX_TMA
+    if ((threadIdx.x & 31) == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(sbkt + kb)) : "memory");
+        sbkt[kb + 1] = 0ull;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+#endif
+}
+
+__device__ __forceinline__ void tma_expect(unsigned long long* mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, unsigned long long* mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_wait(unsigned long long* mbar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(mbar)),
+        "r"(parity)
+        : "memory");
+}
 
 // FINDORPUT of keys q[0, m) (V words each, shared memory), KB at a time.
 // INSERTED keys are written back, compacted, to the front of q (a key is
@@ -172,6 +217,67 @@ __device__ __forceinline__ uint32_t probe_staged(const TableDesc& T, uint32_t* q
             }
             if (!__any_sync(FULLMASK, any)) break;
             __syncwarp();
+            int slot[KPL];
+            uint32_t old[KPL][V];
+#if GX_TMA
+            // one bulk copy per pending key, completing on the warp's
+            // mbarrier (its expected bytes set first by lane 0)
+            {
+                unsigned long long* mbar = sbkt + KB;
+                uint32_t np = 0;
+#pragma unroll
+                for (int i = 0; i < KPL; i++) np += __popc(__ballot_sync(FULLMASK, pend[i]));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic stage use first
+                __syncwarp();
+                if (lane == 0) tma_expect(mbar, np * (uint32_t)(16 * CH));
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < KPL; i++)
+                    if (pend[i]) tma_load(stage + (lane + 32 * i) * CH, T.data + bkt[i] * (uint64_t)BW, 16 * CH, mbar);
+                const uint32_t ph = (uint32_t)sbkt[KB + 1];
+                tma_wait(mbar, ph);
+                __syncwarp();
+                if (lane == 0) sbkt[KB + 1] = ph ^ 1u;
+            }
+            // walk every pending bucket from shared memory: all chunks, each
+            // lane starting at a rotated chunk (conflict-free 16-byte reads
+            // of unswizzled buckets); a match anywhere -> FOUND, else the
+            // lowest EMPTY slot is the CAS candidate (occupied slots are a
+            // prefix, hashtable.py:229-231; a stale view only costs a lost CAS)
+#pragma unroll
+            for (int i = 0; i < KPL; i++) {
+                const uint32_t k = lane + 32 * i;
+                slot[i] = -1;
+                if (!pend[i]) continue;
+                int found = -1, empty = 1 << 20;
+                const int rot = (int)((k * CH) / 8);
+#pragma unroll
+                for (int j = 0; j < CH; j++) {
+                    const int jj = (j + rot) & (CH - 1);
+                    const uint4 c4 = stage[k * CH + jj];
+                    const uint32_t w4[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+                    for (int t = 0; t < SPC; t++) {
+                        bool zero = true, eq = true;
+#pragma unroll
+                        for (int w = 0; w < V; w++) {
+                            zero = zero && w4[t * V + w] == 0u;
+                            eq = eq && w4[t * V + w] == km[i][w];
+                        }
+                        const int sl = jj * SPC + t;
+                        if (eq) found = sl;
+                        if (zero && sl < empty) empty = sl;
+                    }
+                }
+                if (found >= 0) {
+                    rc[i] = FOUND;
+                    slot[i] = found;
+                } else if (empty < S::SPB) {
+                    rc[i] = -3;  // CAS candidate
+                    slot[i] = empty;
+                }
+            }
+#else
             // stage the buckets: chunk c = key c / CH, part c % CH
 #pragma unroll
             for (int it = 0; it < KPL * CH; it++) {
@@ -184,8 +290,6 @@ __device__ __forceinline__ uint32_t probe_staged(const TableDesc& T, uint32_t* q
             cp_async_wait_all();
             __syncwarp();
             // walk each pending bucket from shared memory
-            int slot[KPL];
-            uint32_t old[KPL][V];
 #pragma unroll
             for (int i = 0; i < KPL; i++) {
                 const uint32_t k = lane + 32 * i;
@@ -213,6 +317,7 @@ __device__ __forceinline__ uint32_t probe_staged(const TableDesc& T, uint32_t* q
                     }
                 }
             }
+#endif
             __syncwarp();  // stage and sbkt are free again
             // the candidates' CASes back to back
 #pragma unroll
