@@ -84,13 +84,16 @@ __device__ __forceinline__ void rule_target(const NetDesc& N, const uint4 rl, ui
     }
 }
 
+template <int V, bool EMIT>
+__device__ __forceinline__ void process_rules(const NetDesc& N, const uint32_t* s, const uint4 e, uint64_t& count,
+                                              uint32_t& n, uint32_t lo, uint32_t hi, uint32_t* out);
+
 // The moves of one process in state s: independent moves from qtab entry
 // e, then the rules this process triggers (it is their first participant).
 template <int V, bool EMIT>
 __device__ __forceinline__ void process_moves(const NetDesc& N, const uint32_t* s, const uint4 pr,
                                               const uint4 e, uint64_t& count, uint32_t& n,
                                               uint32_t lo, uint32_t hi, uint32_t* out) {
-    uint32_t t[V];
     count += e.z;
     if (EMIT && n < hi && n + e.y > lo) {
         for (uint32_t d = 0; d < e.y; d++) {
@@ -104,6 +107,14 @@ __device__ __forceinline__ void process_moves(const NetDesc& N, const uint32_t* 
         }
     }
     n += e.y;
+    process_rules<V, EMIT>(N, s, e, count, n, lo, hi, out);
+}
+
+// The rules whose first participant is the process with qtab entry e.
+template <int V, bool EMIT>
+__device__ __forceinline__ void process_rules(const NetDesc& N, const uint32_t* s, const uint4 e, uint64_t& count,
+                                              uint32_t& n, uint32_t lo, uint32_t hi, uint32_t* out) {
+    uint32_t t[V];
     // packed: the trigger count rides in qtab, so states that trigger no
     // rule (most of them) skip the dependent load of the trigger list
     const uint32_t toff = N.trig_packed ? (e.w & 0xffffffu) : e.w;
@@ -172,6 +183,37 @@ __device__ __forceinline__ uint32_t expand_state(const NetDesc& N, const uint32_
                                                  uint32_t* out) {
     uint64_t count = 0;
     uint32_t n = 0;
+    if (N.ngroups) {
+        // grouped: one table lookup per process group; its independent
+        // successors are s with one word XOR-ed; processes that trigger
+        // rules there take the per-process rule path (same successor set
+        // and counts as the loop below, network.py:184-238)
+        for (uint32_t g = 0; g < N.ngroups; g++) {
+            const uint4 gd = N.gdesc[g];
+            const uint32_t wsel = gd.x & 0xffu;
+            const uint4 e = __ldg(&N.gtab[gd.w + ((word_at<V>(s, wsel) >> gd.y) & gd.z)]);
+            count += e.x;
+            if (EMIT && n < hi && n + e.y > lo) {
+                for (uint32_t d = 0; d < e.y; d++) {
+                    const uint32_t idx = n + d;
+                    if (idx < lo || idx >= hi) continue;
+                    const uint32_t dx = __ldg(&N.gdelta[e.z + d]);
+                    uint32_t* o = out + (uint64_t)(idx - lo) * V;
+#pragma unroll
+                    for (int w = 0; w < V; w++) o[w] = (uint32_t)w == wsel ? s[w] ^ dx : s[w];
+                }
+            }
+            n += e.y;
+            for (uint32_t tm = e.w; tm; tm &= tm - 1) {
+                const uint32_t p = ((gd.x >> 8) & 0xffffu) + (uint32_t)(__ffs(tm) - 1);
+                const uint4 pr = proc_desc(N, p);
+                const uint4 qe = __ldg(&N.qtab[pr.w + field_get<V>(s, pr.x, pr.y, pr.z)]);
+                process_rules<V, EMIT>(N, s, qe, count, n, lo, hi, out);
+            }
+        }
+        *count_out = count;
+        return n;
+    }
     for (uint32_t i = 0; i < N.nproc; i++) {
         const uint4 pr = proc_desc(N, i);
         const uint4 e = __ldg(&N.qtab[pr.w + field_get<V>(s, pr.x, pr.y, pr.z)]);

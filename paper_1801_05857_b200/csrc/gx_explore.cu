@@ -829,6 +829,65 @@ int gx_net_create(const gx_network_csr* c, void* stream, gx_net** out) {
             }
         }
     }
+    // process groups for the grouped expansion (gx_internal.h NetDesc):
+    // consecutive processes with adjacent fields in one word, at most
+    // GX_GROUP_BITS bits together; one table entry per joint field code
+    const uint32_t P = c->nproc;
+    std::vector<uint32_t> nst(P);
+    for (uint32_t k = 0; k < P; k++) {
+        const uint32_t qb = c->proc[4 * k + 3];
+        const uint32_t qe = k + 1 < P ? c->proc[4 * (k + 1) + 3] : (uint32_t)(c->n_qtab / 4);
+        nst[k] = qe - qb;
+    }
+    struct Grp { uint32_t word, shift, bits, p0, np; };
+    std::vector<Grp> grps;
+    for (uint32_t k = 0; k < P; k++) {
+        const uint32_t w = c->proc[4 * k], sh = c->proc[4 * k + 1], bits = __builtin_popcount(c->proc[4 * k + 2]);
+        if (!grps.empty()) {
+            Grp& g = grps.back();
+            if (g.word == w && g.shift + g.bits == sh && g.bits + bits <= GX_GROUP_BITS && g.np < 24) {
+                g.bits += bits;
+                g.np++;
+                continue;
+            }
+        }
+        grps.push_back(Grp{w, sh, bits, k, 1});
+    }
+    std::vector<uint32_t> gtab, gdelta;
+    const bool grouped = GX_GROUP_BITS > 0 && grps.size() < P && grps.size() <= GX_GROUP_INLINE;
+    if (grouped) {
+        for (const Grp& g : grps) {
+            for (uint32_t code = 0; code < (1u << g.bits); code++) {
+                uint32_t cnt = 0, ns = 0, tm = 0;
+                const uint32_t off = (uint32_t)gdelta.size();
+                bool valid = true;
+                for (uint32_t k = 0; k < g.np && valid; k++) {
+                    const uint32_t p = g.p0 + k;
+                    const uint32_t sh = c->proc[4 * p + 1], mask = c->proc[4 * p + 2], qb = c->proc[4 * p + 3];
+                    const uint32_t v = (code >> (sh - g.shift)) & mask;
+                    if (v >= nst[p]) {
+                        valid = false;
+                        break;
+                    }
+                    const uint32_t* q = c->qtab + 4ull * (qb + v);  // {im_off, im_n, im_cnt, trig_off}
+                    cnt += q[2];
+                    for (uint32_t d = 0; d < q[1]; d++) gdelta.push_back((v ^ c->im_dst[q[0] + d]) << sh);
+                    ns += q[1];
+                    if (c->trig[q[3]] != 0) tm |= 1u << k;
+                }
+                if (!valid) {
+                    gdelta.resize(off);
+                    cnt = ns = tm = 0;
+                }
+                gtab.insert(gtab.end(), {cnt, ns, off, tm});
+            }
+        }
+    }
+    const uint64_t gt_off = blob.size();
+    blob.insert(blob.end(), gtab.begin(), gtab.end());
+    const uint64_t gd_off = blob.size();
+    blob.insert(blob.end(), gdelta.begin(), gdelta.end());
+    blob.push_back(0u);
     cudaError_t e = cudaMalloc(&n->d_blob, sizeof(uint32_t) * blob.size());
     if (e == cudaSuccess) e = cudaMalloc(&n->d_initial, sizeof(uint32_t) * 16);
     if (e != cudaSuccess) {
@@ -859,6 +918,16 @@ int gx_net_create(const gx_network_csr* c, void* stream, gx_net** out) {
     memset(d.proc_c, 0, sizeof d.proc_c);
     for (uint32_t i = 0; i < c->nproc && i < GX_PROC_INLINE; i++)
         d.proc_c[i] = make_uint4(c->proc[4 * i], c->proc[4 * i + 1], c->proc[4 * i + 2], c->proc[4 * i + 3]);
+    d.gtab = (const uint4*)(n->d_blob + gt_off);
+    d.gdelta = n->d_blob + gd_off;
+    d.ngroups = grouped ? (uint32_t)grps.size() : 0u;
+    memset(d.gdesc, 0, sizeof d.gdesc);
+    uint32_t base = 0;
+    for (size_t g = 0; grouped && g < grps.size(); g++) {
+        d.gdesc[g] = make_uint4(grps[g].word | grps[g].p0 << 8 | grps[g].np << 24, grps[g].shift,
+                                (1u << grps[g].bits) - 1u, base);
+        base += 1u << grps[g].bits;
+    }
     *out = n;
     return GX_OK;
 }

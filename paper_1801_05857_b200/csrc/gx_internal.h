@@ -35,6 +35,10 @@ int sm_count();
 
 // Device network, network.py:43-62 flattened (see gx.h gx_network_csr).
 #define GX_PROC_INLINE 32  // processes whose descriptors ride in the kernel parameters
+#define GX_GROUP_INLINE 32  // process groups the grouped expansion supports (else per process)
+#ifndef GX_GROUP_BITS
+#define GX_GROUP_BITS 10    // joint field bits per group table (2^bits entries of 16 bytes)
+#endif
 
 struct NetDesc {
     const uint4* proc;   // {word, shift, mask, qbase}
@@ -53,6 +57,15 @@ struct NetDesc {
     // (constant) bank: the expansion loop walks them in lockstep across the
     // warp, so a uniform constant load replaces an L1 round trip
     uint4 proc_c[GX_PROC_INLINE];
+    // process groups (gx_net_create): runs of consecutive processes whose
+    // fields are adjacent in one word, looked up together -- one table
+    // entry per joint local-state code gives the group's transition count,
+    // independent successors (XOR deltas in gdelta) and which of its
+    // processes trigger rules.  ngroups = 0: the per-process loop.
+    const uint4* gtab;       // {count, nsucc, delta_off, trigger mask}
+    const uint32_t* gdelta;  // independent successors as XOR masks of the group's word
+    uint32_t ngroups, pad_g[3];
+    uint4 gdesc[GX_GROUP_INLINE];  // {word | p0 << 8 | np << 24, shift, mask, gtab base}
 };
 
 // A growable device scratch buffer.

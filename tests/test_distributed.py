@@ -318,3 +318,151 @@ def test_fused_driver_matches_single_process():
                 assert dig == ref.table.digest(), (name, world)
             if job[2] is None:
                 assert sorted(map(list, dls)) == sorted(models[name]["bfs"]["deadlocks"])[:100], name
+
+
+# ------------------------------------- partitioned (dedup) driver protocol
+
+class OraclePartShard(OracleFusedShard):
+    """CPU stand-in for a FusedShard in the partitioned dedup mode: the
+    expansion routes EVERY successor (own ones too) and touches no table;
+    chunk_status flags an inbox overflow when a chunk sends more than
+    inbox/world keys to one owner (the device flags the receiver's
+    reservation), and rollback discards the chunk; absorb_chunk exchanges,
+    de-duplicates (the L2 set) and inserts.  Exercises ChunkPlanner and
+    _level_partitioned, including repeated rollbacks, over gloo."""
+
+    def __init__(self, path, table_kw, world, rank, inbox=48):
+        super().__init__(path, table_kw, world, rank)
+        from types import SimpleNamespace
+
+        from paper_1801_05857_b200 import load_network
+        self.dedup = True
+        self.inbox_capacity = inbox
+        self.set_slots = 64
+        self.dnet = SimpleNamespace(net=load_network(path))
+        self.rollbacks = 0
+        self.nsubs = []
+
+    def set_partitions(self, nsub):
+        assert nsub & (nsub - 1) == 0
+        self.nsubs.append(nsub)
+
+    def expand_range(self, begin, count):
+        b = self.base
+        rows = self.front[begin:begin + count]
+        self.c_exp, self.c_trans, self.c_dl, self.c_kept = len(rows), 0, 0, []
+        succ = []
+        for row in rows:
+            out, c = b.net.expand(b.net.unpack(row))
+            self.c_trans += c
+            if not out and self.detect:
+                self.c_dl += 1
+                self.c_kept.append(b.net.unpack(row))
+            succ += [b.net.pack(t) for _, t in out]
+        arr = np.array(succ, np.uint32).reshape(-1, self.vlen)
+        own = b.owner(arr) if len(arr) else np.zeros(0, np.int64)
+        self.outgoing = [arr[own == r] for r in range(self.world)]
+        self.c_ovf = int(any(len(x) > self.inbox_capacity // self.world for x in self.outgoing))
+        self.c_routed = len(arr)
+
+    def chunk_status(self):
+        # cumulative counters as the device reports them (this chunk included)
+        return np.array([self.c_ovf, getattr(self, "routed_total", 0) + self.c_routed,
+                         self.expanded + self.c_exp], np.uint64)
+
+    def rollback(self):
+        self.rollbacks += 1
+        self.outgoing = [np.zeros((0, self.vlen), np.uint32)] * self.world
+
+    def absorb_chunk(self):
+        b = self.base
+        self.expanded += self.c_exp
+        self.trans += self.c_trans
+        self.dl_total += self.c_dl
+        self.kept += self.c_kept
+        self.routed_total = getattr(self, "routed_total", 0) + self.c_routed
+        counts = torch.tensor([len(x) for x in self.outgoing], dtype=torch.int64)
+        rc = torch.empty_like(counts)
+        dist.all_to_all_single(rc, counts)
+        send = torch.from_numpy(np.concatenate(self.outgoing).astype(np.int32).reshape(-1, self.vlen))
+        recv = torch.empty((int(rc.sum()), self.vlen), dtype=torch.int32)
+        dist.all_to_all_single(recv, send, output_split_sizes=rc.tolist(), input_split_sizes=counts.tolist())
+        keys = recv.numpy().astype(np.uint32)
+        if len(keys):
+            keys = np.unique(keys, axis=0)  # the duplicate filter
+            codes, _ = b.table.find_or_insert_batch(keys)
+            self.next.append(keys[codes == 1])
+            self.full |= bool((codes == 2).any())
+        self.outgoing = [np.zeros((0, self.vlen), np.uint32)] * self.world
+
+    def end_level(self):
+        st = super().end_level()
+        st[6] = getattr(self, "routed_total", 0)
+        return st
+
+
+def _part_worker(rank, world, port, jobs, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1801_05857_b200.distributed import explore_fused
+    out = []
+    try:
+        for name, table_kw in jobs:
+            s = OraclePartShard(model_path(name), table_kw, world, rank)
+            r = explore_fused(s, dist, torch, True, device=torch.device("cpu"))
+            out.append((name, r.states, r.transitions, r.iterations, r.deadlocks_total, r.outcome,
+                        r.digest, s.rollbacks, max(s.nsubs)))
+    except Exception as err:  # noqa: BLE001 - surfaced to the parent
+        q.put(repr(err))
+        raise
+    if rank == 0:
+        q.put(out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_partitioned_driver_chunks_and_rollbacks():
+    """_level_partitioned + ChunkPlanner over gloo (world 2): tiny inboxes
+    force many chunks, overflowing chunks are rolled back and re-run, and
+    the results equal the single-process reference engine's."""
+    from oracle import oracle as O
+    jobs = [("ring8", {"capacity_words": 1 << 18}), ("gas6", {"capacity_words": 1 << 18}),
+            ("phil5", {"capacity_words": 1 << 16}), ("sinks8", {"capacity_words": 1 << 16})]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_part_worker, args=(r, 2, port, jobs, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+    assert not isinstance(res, str), res
+    rolled = 0
+    for (name, states, trans, iters, dl, outcome, dig, rb, nsub), job in zip(res, jobs):
+        ref = O.explore(O.Net.from_file(model_path(name)), capacity_words=job[1]["capacity_words"],
+                        detect_deadlocks=True)
+        assert (states, trans, iters, dl, outcome) == \
+            (ref.states, ref.transitions, ref.iterations, ref.deadlocks_total, ref.outcome), name
+        assert dig == ref.table.digest(), name
+        rolled += rb
+    assert rolled > 0  # the overflow path ran
+
+
+def test_chunk_planner_sizes():
+    from types import SimpleNamespace
+
+    from paper_1801_05857_b200 import load_network
+    from paper_1801_05857_b200.distributed import ChunkPlanner
+    net = load_network(model_path("ring8"))
+    sh = SimpleNamespace(world=2, inbox_capacity=1 << 20, set_slots=1 << 22, dnet=SimpleNamespace(net=net))
+    p = ChunkPlanner([sh, sh])
+    first = p.chunk()
+    assert first == int(0.8 * (1 << 20) / p.ratio)
+    p.observe(routed=5 * 1000, expanded=1000)        # 5 successors per state seen
+    assert abs(p.ratio - (1.2 * 5 + 0.5)) < 1e-9 and p.chunk() > first
+    p.overflowed()
+    assert abs(p.ratio - 2 * (1.2 * 5 + 0.5)) < 1e-9
+    assert p.nsub(10) == 1
+    big = p.nsub(10 ** 9)
+    assert big & (big - 1) == 0 and big == p.nsub_max == 64
