@@ -131,7 +131,7 @@ __device__ __forceinline__ void process_rules(const NetDesc& N, const uint32_t* 
             if (!combos) break;
         }
         if (!combos) continue;
-        const uint32_t nd = __ldg(&N.dedup[rl.z]);
+        const uint32_t nd = rl.z ? __ldg(&N.dedup[rl.z]) : 0u;  // offset 0: the empty list
         if (nd == 0) {
             count += combos;
             if (EMIT && n < hi && n + combos > lo) {

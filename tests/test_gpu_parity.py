@@ -364,8 +364,11 @@ def test_device_bench_reference_pins(bw, vlen):
             occ = t.occupancy()[0]
         finally:
             t.close()
-        if r["full"]:  # vlen 2 at bw 4: 2 slots per bucket at 50% load
-            assert bw == 4 and vlen == 2
+        if r["full"]:
+            # the reference's sizing (<= 50% load at d = 1, K = 8) overfills
+            # buckets of <= 4 slots at these sizes: bw 4 / vlen 1,
+            # bw 4 and 8 / vlen 2
+            assert bw // vlen <= 4, (bw, vlen, total, d)
             continue
         assert (r["found"], r["inserted"], occ) == (total - total // d, total // d, total // d), (total, d)
         if (total, d) == (5000, 10):
