@@ -34,9 +34,6 @@
 #ifndef GX_STAGE_KB_MAX
 #define GX_STAGE_KB_MAX 32  // keys per staged batch at most (B200 sweeps: 3 blocks x 32 > 2 blocks x 64)
 #endif
-#ifndef GX_STAGE_PERLANE
-#define GX_STAGE_PERLANE 0  // 1: each lane stages its own bucket (8 uncoalesced 16-byte copies)
-#endif
 #ifndef GX_TMA
 #define GX_TMA 0  // 1: stage buckets with one bulk copy (TMA) per key instead of BW/4 cp.async (B200: 5-10% slower, profiles/README.md)
 #endif
@@ -281,21 +278,6 @@ __device__ __forceinline__ uint32_t probe_staged(const TableDesc& T, uint32_t* q
                 }
             }
 #else
-#if GX_STAGE_PERLANE
-            // stage the buckets: each lane copies its own keys' buckets
-            // (chunk j of key k to k*CH + (j ^ (k & (CH-1))), the swizzle the
-            // walk reads conflict-free): one base address per key instead of
-            // a shared-memory index lookup and address per 16-byte chunk
-#pragma unroll
-            for (int i = 0; i < KPL; i++) {
-                if (!pend[i]) continue;
-                const uint32_t k = lane + 32 * i;
-                const uint32_t* src = T.data + bkt[i] * (uint64_t)BW;
-                uint4* dst = stage + k * CH;
-#pragma unroll
-                for (int j = 0; j < CH; j++) cp_async16(dst + (j ^ (k & (CH - 1))), src + 4 * j);
-            }
-#else
             // stage the buckets: chunk c = key c / CH, part c % CH
 #pragma unroll
             for (int it = 0; it < KPL * CH; it++) {
@@ -305,7 +287,7 @@ __device__ __forceinline__ uint32_t probe_staged(const TableDesc& T, uint32_t* q
                 if (b != SKIP)
                     cp_async16(stage + k * CH + (j ^ (k & (CH - 1))), T.data + b * (uint64_t)BW + 4 * j);
             }
-#endif
+
             cp_async_wait_all();
             __syncwarp();
             // walk each pending bucket from shared memory
