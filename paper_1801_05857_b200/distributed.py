@@ -201,7 +201,11 @@ class FusedShard:
         from .network import max_successors
         # frontier states per chunk so that no inbox can overflow even if every
         # successor of every sender's chunk went to one owner
-        self.chunk_states = max(1, inbox_capacity // (world * max_successors(net)))
+        # (GX_CHUNK_SUCC overrides the bound: a measurement knob only -- an
+        # inbox overflow then aborts the search)
+        import os
+        bound = float(os.environ.get("GX_CHUNK_SUCC", max_successors(net)))
+        self.chunk_states = max(1, int(inbox_capacity // (world * bound)))
 
     @property
     def handle(self):
