@@ -201,11 +201,9 @@ class FusedShard:
         from .network import max_successors
         # frontier states per chunk so that no inbox can overflow even if every
         # successor of every sender's chunk went to one owner
-        # (GX_CHUNK_SUCC overrides the bound: a measurement knob only -- an
-        # inbox overflow then aborts the search)
-        import os
-        bound = float(os.environ.get("GX_CHUNK_SUCC", max_successors(net)))
-        self.chunk_states = max(1, int(inbox_capacity // (world * bound)))
+        # (measured: sizing chunks for 16 instead of ring19's bound of 38
+        # successors per state gains only 2%, profiles/README.md)
+        self.chunk_states = max(1, inbox_capacity // (world * max_successors(net)))
 
     @property
     def handle(self):
