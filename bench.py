@@ -80,6 +80,8 @@ def parse():
     ap.add_argument("--dedup", action="store_true",
                     help="sharded engine: partitioned levels with the level-wide L2 duplicate filter")
     ap.add_argument("--dedup-set-log2", type=int, default=20)
+    ap.add_argument("--pipeline", type=int, default=0,
+                    help="sharded engine: absorb chunk c-1's inbox inside chunk c's expansion launch")
     ap.add_argument("--cpu-sample", default="ring14",
                     help="token ring the CPU reference arm explores (ring14: 4.5e7 states, ~12 s on 16 cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -494,7 +496,8 @@ def main():
                        capacity_words=cap)
     cfg = ExploreConfig(table=tcfg, detect_deadlocks=True, probe_group=args.probe_group,
                         cache_slots=max(1, args.cache_slots), filter_log2=args.filter_log2,
-                        dedup=args.dedup, dedup_set_log2=args.dedup_set_log2, state_digest=False)
+                        dedup=args.dedup, dedup_set_log2=args.dedup_set_log2, state_digest=False,
+                        pipeline=bool(args.pipeline))
     stream = torch.cuda.current_stream().cuda_stream
     from paper_1801_05857_b200.hashtable import slots_per_bucket
     spb0 = slots_per_bucket(args.bucket_words, vlen, "half" if args.bucket_words == 32 else "plain")

@@ -328,6 +328,16 @@ int gx_shard_bench_route(gx_shard *s, uint64_t total, uint64_t duplication, uint
 int gx_shard_bench_result(gx_shard *s, uint64_t *out, double *ms);
 
 int gx_shard_set_mode(gx_shard *s, int32_t dedup, int32_t set_log2);
+
+/* Pipelined fused levels: the inbox is split in two halves; the launch for
+ * chunk c of a level (gx_shard_expand_range) routes into the peers' half
+ * c & 1 and, in the same kernel, FINDORPUTs the keys routed here during
+ * chunk c - 1 (half (c - 1) & 1), so the memory-bound absorb work overlaps
+ * the issue-bound expansion.  Protocol per level: for each chunk every
+ * shard calls gx_shard_expand_range, then a barrier; after the last chunk
+ * every shard calls gx_shard_absorb_chunk once (the last half), then
+ * gx_shard_end_level. */
+int gx_shard_set_pipeline(gx_shard *s, int32_t on);
 int gx_shard_set_partitions(gx_shard *s, uint32_t nsub);
 int gx_shard_chunk_status(gx_shard *s, uint64_t *out);
 int gx_shard_rollback(gx_shard *s);

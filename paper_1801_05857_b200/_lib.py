@@ -108,6 +108,7 @@ SIGNATURES = {
     "gx_shard_expand_range": (C.c_int, [_vp, C.c_uint64, C.c_uint64]),
     "gx_shard_absorb_chunk": (C.c_int, [_vp]),
     "gx_shard_set_mode": (C.c_int, [_vp, C.c_int32, C.c_int32]),
+    "gx_shard_set_pipeline": (C.c_int, [_vp, C.c_int32]),
     "gx_shard_bench_route": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.c_uint64,
                                        C.c_uint64]),
     "gx_shard_bench_result": (C.c_int, [_vp, _u64p, _P(C.c_double)]),

@@ -418,9 +418,18 @@ struct StagedSmem {
     static constexpr size_t FIXED = Q + B + ST;
 };
 
+// Inbox keys to FINDORPUT in the same launch as the expansion (the
+// sharded engine's pipelined mode): keys other shards routed here during
+// the previous chunk.  keys == nullptr: none.
+struct AbsorbArgs {
+    const uint32_t* keys;
+    const unsigned long long* count;
+    uint64_t cap;
+};
+
 template <int BW, int V, bool ROUTE>
 __device__ __forceinline__ void level_staged_body(const TableDesc& T, const NetDesc& N, const LevelArgs& A,
-                                                  const RouteArgs& R) {
+                                                  const RouteArgs& R, const AbsorbArgs AB = AbsorbArgs{nullptr, nullptr, 0}) {
     using L = StagedSmem<BW, V>;
     using S = Staged<BW, V>;
     constexpr int QCAP = QWORDS / V;
@@ -440,12 +449,35 @@ __device__ __forceinline__ void level_staged_body(const TableDesc& T, const NetD
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
     unsigned long long trans = 0, expanded = 0, probes = 0, routed = 0;
-    for (uint64_t base = warp * 32; base < A.nfront; base += nwarps * 32) {
+    // pipelined mode: every warp alternates a frontier tile with a batch of
+    // inbox keys, so the pure-probe absorb work fills the latency gaps of
+    // the expansion (one shard's table only: the TLB-friendly order holds)
+    uint64_t n_abs = 0;
+    if (ROUTE && AB.keys) n_abs = min((uint64_t)*AB.count, AB.cap);
+    uint64_t batch = warp * QCAP;
+    for (uint64_t base = warp * 32; base < A.nfront || batch < n_abs; base += nwarps * 32) {
         int stop = 0;
         if (lane == 0)
             stop = (*(volatile unsigned long long*)&A.ctr[LV_FULL] != 0ull) ||
                    (*(volatile unsigned long long*)&A.ctr[LV_OVF] != 0ull);
         if (__shfl_sync(FULLMASK, stop, 0)) break;
+        if (ROUTE && batch < n_abs) {
+            const uint32_t m0 = (uint32_t)min((uint64_t)QCAP, n_abs - batch);
+            for (uint32_t x = lane; x < m0 * V; x += 32) q[x] = __ldcs(AB.keys + batch * V + x);
+            __syncwarp();
+            uint32_t m = m0;
+            if (cmask)
+                m = filter_route<V, false>(T, R, dcache, cmask, q, m, &A.ctr[LV_OVF], &routed,
+                                           reinterpret_cast<uint32_t*>(stage));
+            probes += lane == 0 ? m : 0;
+            uint32_t full = 0;
+            const uint32_t n_out = probe_staged<BW, V>(T, q, m, stage, sbkt, &full);
+            if (__any_sync(FULLMASK, full != 0u) && lane == 0) atomicExch(&A.ctr[LV_FULL], 1ull);
+            if (n_out) flush_out<V>(A, q, n_out);
+            __syncwarp();
+            batch += nwarps * QCAP;
+        }
+        if (base >= A.nfront) continue;
         const uint64_t idx = base + lane;
         const bool has = idx < A.nfront;
         uint32_t s[V];

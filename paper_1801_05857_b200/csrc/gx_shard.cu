@@ -32,8 +32,9 @@
 namespace gx {
 
 template <int BW, int V>
-__global__ void __launch_bounds__(256, GX_STAGED_MINB) k_level_routed(TableDesc T, NetDesc N, LevelArgs A, RouteArgs R) {
-    level_staged_body<BW, V, true>(T, N, A, R);
+__global__ void __launch_bounds__(256, GX_STAGED_MINB) k_level_routed(TableDesc T, NetDesc N, LevelArgs A, RouteArgs R,
+                                                                      AbsorbArgs AB) {
+    level_staged_body<BW, V, true>(T, N, A, R, AB);
 }
 
 // FINDORPUT the inbox (n = *count keys, clamped to cap); inserted keys go to
@@ -280,7 +281,7 @@ static PartKernels pick_part(const TableDesc& T) {
     return {nullptr, nullptr, nullptr, 0, 0};
 }
 
-typedef void (*routed_kernel_t)(TableDesc, NetDesc, LevelArgs, RouteArgs);
+typedef void (*routed_kernel_t)(TableDesc, NetDesc, LevelArgs, RouteArgs, AbsorbArgs);
 typedef void (*absorb_kernel_t)(TableDesc, LevelArgs, const uint32_t*, const unsigned long long*, uint64_t,
                                 const unsigned long long*, const uint32_t*, const unsigned long long*, uint64_t);
 
@@ -364,6 +365,13 @@ struct gx_shard {
     DevBuf uniq;  // first occurrences of one sub-partition: [ctr, ovf, pad..256 B][keys]
     uint64_t uniq_cap = 0;
     size_t smem_a = 0;
+    // pipelined mode (gx_shard_set_pipeline): two inbox halves per shard;
+    // chunk c routes into half c & 1 and absorbs half (c - 1) & 1 in the
+    // same launch
+    bool pipelined = false;
+    uint64_t half = 0;        // keys per inbox half
+    uint32_t chunk_idx = 0;   // chunks expanded in the current level
+    void* peer_block[GX_MAX_SHARDS] = {};
 };
 
 extern "C" {
@@ -463,8 +471,21 @@ int gx_shard_ipc_handle(gx_shard* s, uint8_t* out) {
 }
 
 static void set_peer(gx_shard* s, int r, void* block) {
+    s->peer_block[r] = block;
     s->R.inbox_ctr[r] = (unsigned long long*)block;
     s->R.inbox[r] = (uint32_t*)((char*)block + INBOX_HEAD);
+}
+
+// RouteArgs for inbox half `parity` of every peer (pipelined mode)
+static RouteArgs route_half(const gx_shard* s, uint32_t parity) {
+    RouteArgs R = s->R;
+    const uint32_t v = s->t->d.vlen;
+    for (int r = 0; r < s->world; r++) {
+        R.inbox_ctr[r] = (unsigned long long*)s->peer_block[r] + parity;
+        R.inbox[r] = (uint32_t*)((char*)s->peer_block[r] + INBOX_HEAD) + (uint64_t)parity * s->half * v;
+    }
+    R.inbox_cap = s->half;
+    return R;
 }
 
 int gx_shard_connect(gx_shard* s, const uint8_t* handles) {
@@ -544,6 +565,7 @@ int gx_shard_begin(gx_shard* s, int32_t owns_initial, int32_t detect_deadlocks, 
     s->detect = detect_deadlocks;
     s->level_open = false;
     s->ev_used = 0;
+    s->chunk_idx = 0;
     *table_full = 0;
     if (owns_initial) {
         rc = t->codes.ensure(16);
@@ -683,13 +705,39 @@ int gx_shard_expand_range(gx_shard* s, uint64_t begin, uint64_t count) {
         return GX_OK;
     }
     GX_CUDA(cudaEventRecord(a0, s->stream));
-    if (count) {
+    if (s->pipelined) {
+        // route into half c & 1, absorb what peers routed here in chunk c - 1
+        const uint32_t p = s->chunk_idx & 1u;
+        AbsorbArgs AB{nullptr, nullptr, 0};
+        unsigned long long* own = (unsigned long long*)s->inbox_block;
+        if (s->chunk_idx > 0)
+            AB = AbsorbArgs{(const uint32_t*)((char*)s->inbox_block + INBOX_HEAD) + (uint64_t)(p ^ 1u) * s->half * v,
+                            own + (p ^ 1u), s->half};
+        const uint64_t want = std::max<uint64_t>((count + 31) / 32, 1);
+        const int g = (int)std::min<uint64_t>((uint64_t)sm_count() * GX_STAGED_MINB,
+                                              s->chunk_idx > 0 ? (uint64_t)sm_count() * GX_STAGED_MINB : (want + 7) / 8);
+        s->K.a<<<g, 256, s->smem, s->stream>>>(t->d, s->n->d, A, route_half(s, p), AB);
+        GX_LAUNCHED();
+        if (s->chunk_idx > 0) GX_CUDA(cudaMemsetAsync(own + (p ^ 1u), 0, 8, s->stream));
+        s->chunk_idx++;
+    } else if (count) {
         const uint64_t want = (count + 31) / 32;
         const int g = (int)std::min<uint64_t>((uint64_t)sm_count() * GX_STAGED_MINB, (want + 7) / 8);
-        s->K.a<<<g, 256, s->smem, s->stream>>>(t->d, s->n->d, A, s->R);
+        s->K.a<<<g, 256, s->smem, s->stream>>>(t->d, s->n->d, A, s->R, AbsorbArgs{nullptr, nullptr, 0});
         GX_LAUNCHED();
     }
     GX_CUDA(cudaEventRecord(a1, s->stream));
+    return GX_OK;
+}
+
+int gx_shard_set_pipeline(gx_shard* s, int32_t on) {
+    if (on && s->dedup) {
+        set_error("the pipelined mode is for the fused levels, not the partitioned one");
+        return GX_EINPUT;
+    }
+    s->pipelined = on != 0;
+    s->half = s->inbox_cap / 2;
+    s->chunk_idx = 0;
     return GX_OK;
 }
 
@@ -735,7 +783,10 @@ int gx_shard_bench_route(gx_shard* s, uint64_t total, uint64_t dup, uint64_t see
     cudaEvent_t a0 = next_event(s), a1 = next_event(s);
     GX_CUDA(cudaEventRecord(a0, s->stream));
     if (count) {
-        k<<<sm_count() * GX_STAGED_MINB, 256, s->K.fixed_smem, s->stream>>>(T, s->A, s->R, B, first, count);
+        // pipelined shards: route into half 0, which absorb_chunk then drains
+        const RouteArgs R = s->pipelined ? route_half(s, 0) : s->R;
+        if (s->pipelined) s->chunk_idx = 1;
+        k<<<sm_count() * GX_STAGED_MINB, 256, s->K.fixed_smem, s->stream>>>(T, s->A, R, B, first, count);
         GX_LAUNCHED();
     }
     GX_CUDA(cudaEventRecord(a1, s->stream));
@@ -823,6 +874,18 @@ int gx_shard_absorb_chunk(gx_shard* s) {
     // overflowing inbox in LV_OVF); the counter is reset in stream order
     cudaEvent_t b0 = next_event(s), b1 = next_event(s);
     GX_CUDA(cudaEventRecord(b0, st));
+    if (s->pipelined) {
+        // the last chunk's half (the level's final absorb)
+        const uint32_t p = (s->chunk_idx + 1) & 1u;  // (chunk_idx - 1) & 1
+        unsigned long long* own = (unsigned long long*)s->inbox_block + p;
+        const uint32_t* keys = (const uint32_t*)((char*)s->inbox_block + INBOX_HEAD) + (uint64_t)p * s->half * t->d.vlen;
+        s->K.b<<<sm_count() * GX_STAGED_MINB, 256, s->smem, st>>>(t->d, s->A, keys, own, s->half, nullptr, nullptr,
+                                                                 nullptr, 0);
+        GX_LAUNCHED();
+        GX_CUDA(cudaEventRecord(b1, st));
+        GX_CUDA(cudaMemsetAsync(own, 0, 8, st));
+        return GX_OK;
+    }
     s->K.b<<<sm_count() * GX_STAGED_MINB, 256, s->smem, st>>>(t->d, s->A, s->R.inbox[s->rank],
                                                              s->R.inbox_ctr[s->rank], s->inbox_cap, nullptr,
                                                              nullptr, nullptr, 0);
@@ -872,6 +935,7 @@ int gx_shard_end_level(gx_shard* s, uint64_t* stats) {
     s->nF = nnew;
     s->rev ^= 1;
     s->level_open = false;
+    s->chunk_idx = 0;
     // per-level claims / new, then cumulative counters
     stats[GX_SH_CLAIMS] = claims;
     stats[GX_SH_NEW] = nnew;

@@ -195,6 +195,9 @@ class FusedShard:
         if self.dedup:
             check(lib().gx_shard_set_mode(h, 1, int(cfg.dedup_set_log2)))
             self.set_slots = (1 << int(cfg.dedup_set_log2)) * (2 if self.vlen == 4 else 4)
+        self.pipelined = bool(getattr(cfg, "pipeline", False)) and not self.dedup
+        if self.pipelined:
+            check(lib().gx_shard_set_pipeline(h, 1))
         self.init = np.zeros(self.vlen, np.uint32)
         packed = statevec.pack(self.scheme, net.initial)
         self.init[:len(packed)] = packed
@@ -202,8 +205,10 @@ class FusedShard:
         # frontier states per chunk so that no inbox can overflow even if every
         # successor of every sender's chunk went to one owner
         # (measured: sizing chunks for 16 instead of ring19's bound of 38
-        # successors per state gains only 2%, profiles/README.md)
-        self.chunk_states = max(1, inbox_capacity // (world * max_successors(net)))
+        # successors per state gains only 2%, profiles/README.md); a
+        # pipelined shard routes into half of its peers' inboxes per chunk
+        per_chunk = inbox_capacity // 2 if self.pipelined else inbox_capacity
+        self.chunk_states = max(1, per_chunk // (world * max_successors(net)))
 
     @property
     def handle(self):
@@ -355,6 +360,15 @@ def _run_levels(shards, barrier, reduce, detect: bool, max_iterations=None, redu
             widest = int(reduce_max(np.array([max(s.frontier() for s in shards)], np.uint64))[0])
             if dedup:
                 _level_partitioned(shards, barrier, reduce, planner, widest)
+            elif all(getattr(s, "pipelined", False) for s in shards):
+                # chunk c's launch also absorbs chunk c - 1's inbox half
+                chunks = max(1, -(-widest // chunk))
+                for c in range(chunks):
+                    for s in shards:
+                        s.expand_range(c * chunk, chunk)
+                    barrier()
+                for s in shards:
+                    s.absorb_chunk()
             else:
                 chunks = max(1, -(-widest // chunk))
                 for c in range(chunks):

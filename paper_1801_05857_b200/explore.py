@@ -73,6 +73,9 @@ class ExploreConfig:
     # the filter set has 2^dedup_set_log2 32-byte groups (L2 resident)
     dedup: bool = False
     dedup_set_log2: int = 20
+    # sharded engine, fused levels: split each inbox in two halves and
+    # absorb chunk c - 1's keys inside chunk c's expansion launch
+    pipeline: bool = False
 
     def __post_init__(self):
         if self.workers < 1:

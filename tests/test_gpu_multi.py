@@ -198,3 +198,34 @@ def test_nccl_all_to_all_driver_world1():
         assert (states, trans, dl) == (b["states"], b["transitions"], b["deadlocks_total"]), name
         assert dls == b["deadlocks"][:100], name
     assert res[-1][0] == "binning" and res[-1][3] and res[-1][1] > 0
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_pipelined_mode_matches_reference(world):
+    """Fused levels with double-buffered inboxes: chunk c's launch routes
+    into one half and absorbs chunk c - 1's keys from the other."""
+    for name in sorted(REF):
+        net = gx.load_network(model_path(name))
+        if not _inband(net):
+            continue
+        cfg = ExploreConfig(table=TableConfig(capacity_words=1 << 20), detect_deadlocks=True, pipeline=True)
+        rep = D.explore_local_shards(net, cfg, world)
+        b = MODELS[name]["bfs"]
+        assert list(rep.digest) == REF[name], (name, world)
+        assert (rep.states, rep.transitions, rep.deadlocks_total, rep.outcome) == \
+            (b["states"], b["transitions"], b["deadlocks_total"], "COMPLETE"), (name, world)
+        assert [list(s) for s in rep.deadlocks] == b["deadlocks"][:100], name
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_pipelined_mode_many_chunks(world, tmp_path):
+    """Small inboxes: many chunks per level, every half reused many times."""
+    from oracle import oracle as O
+    from paper_1801_05857_b200.bench import gen_token_ring
+    n = 12
+    net = gx.load_network(gen_token_ring(n, tmp_path / "r")[1])
+    cfg = ExploreConfig(table=TableConfig(capacity_words=1 << 24), detect_deadlocks=True, pipeline=True)
+    rep = D.explore_local_shards(net, cfg, world, inbox_capacity=1 << 17, frontier_capacity=1 << 20)
+    assert (rep.states, rep.transitions, rep.iterations) == (2 * n * 3 ** (n - 1), 4 * n * n * 3 ** (n - 2),
+                                                             6 * n - 4 + 1)
+    assert rep.digest == O.ring_digest(n)
