@@ -567,6 +567,10 @@ __global__ void __launch_bounds__(256) k_bench(TableDesc T, BenchArgs B) {
 
 typedef void (*bench_kernel_t)(TableDesc, BenchArgs);
 
+#ifndef GX_BENCH_BATCH
+#define GX_BENCH_BATCH 512  // keys generated per warp per probe call
+#endif
+
 // The same benchmark on the staged probe (the level kernel's FINDORPUT):
 // each warp generates KB keys into its shared-memory queue and resolves
 // them with probe_staged.  Counts INSERTED / TABLE_FULL.
@@ -574,19 +578,20 @@ template <int BW, int V>
 __global__ void __launch_bounds__(256, 2) k_bench_staged(TableDesc T, BenchArgs B) {
     using S = Staged<BW, V>;
     constexpr int KB = S::KB;
+    constexpr int BQ = GX_BENCH_BATCH;  // keys per warp per probe call (the refill probe keeps 32 lanes busy)
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * (KB * V);
-    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + 8ull * KB * V * 4) + wid * S::SB_STRIDE;
-    uint4* stage = reinterpret_cast<uint4*>(smem + 8ull * KB * V * 4 + 8ull * S::SB_STRIDE * 8 +
+    uint32_t* q = reinterpret_cast<uint32_t*>(smem) + wid * (BQ * V);
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + 8ull * BQ * V * 4) + wid * S::SB_STRIDE;
+    uint4* stage = reinterpret_cast<uint4*>(smem + 8ull * BQ * V * 4 + 8ull * S::SB_STRIDE * 8 +
                                             (size_t)wid * S::STAGE_BYTES);
     staged_init(sbkt, KB);
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
     unsigned long long ins = 0, full = 0, loads = 0;
-    for (uint64_t base = warp * KB; base < B.total; base += nwarps * KB) {
-        const uint32_t m = (uint32_t)min((uint64_t)KB, B.total - base);
+    for (uint64_t base = warp * BQ; base < B.total; base += nwarps * BQ) {
+        const uint32_t m = (uint32_t)min((uint64_t)BQ, B.total - base);
         for (uint32_t k = lane; k < m; k += 32) {
             uint32_t key[V];
             bench_key<V>(B, base + k, key);
@@ -614,7 +619,7 @@ __global__ void __launch_bounds__(256, 2) k_bench_staged(TableDesc T, BenchArgs 
 template <int BW, int V>
 static size_t bench_staged_smem() {
     using S = Staged<BW, V>;
-    return 8ull * S::KB * V * 4 + 8ull * S::SB_STRIDE * 8 + 8ull * S::STAGE_BYTES;
+    return 8ull * GX_BENCH_BATCH * V * 4 + 8ull * S::SB_STRIDE * 8 + 8ull * S::STAGE_BYTES;
 }
 
 struct BenchKernel {

@@ -169,6 +169,138 @@ __device__ __forceinline__ void tma_wait(unsigned long long* mbar, uint32_t pari
         : "memory");
 }
 
+#ifndef GX_REFILL
+#define GX_REFILL 1  // one key per lane, lanes refilled as their keys resolve (see probe_refill)
+#endif
+
+// FINDORPUT of keys q[0, m) with every lane owning one key at a time and a
+// round = one bucket per lane: all 32 buckets of a round are staged with
+// cp.async at once, each lane resolves its key from shared memory, and a
+// lane whose key is done (FOUND, INSERTED, TABLE_FULL) takes the next key
+// of q while the lanes whose bucket was full go on to their next hash
+// function in the same round.  The batch-synchronous version
+// (probe_staged below with GX_REFILL 0) ran a whole extra memory round
+// for the few keys of a batch of 32 that needed a second bucket -- at load
+// 0.75, 95% of batches; here those keys share a round with fresh keys.
+// Same results: each key's probe sequence and CAS protocol are unchanged
+// (hashtable.py:224-280).  INSERTED keys are written, compacted, to the
+// front of q (always below the next key to read); returns their number.
+template <int BW, int V>
+__device__ __forceinline__ uint32_t probe_refill(const TableDesc& T, uint32_t* q, uint32_t m, uint4* stage,
+                                                 unsigned long long* sbkt, uint32_t* full,
+                                                 uint32_t* nprobe = nullptr) {
+    constexpr int CH = BW / 4, SPC = 4 / V;
+    constexpr unsigned long long SKIP = ~0ull;
+    const int lane = threadIdx.x & 31;
+    const uint32_t mark_lo = T.mark;
+    uint32_t n_ins = 0;
+    // lane state: its key (with the mark), fold, hash function index
+    uint32_t km[V];
+    uint64_t h = 0;
+    int r = 0;
+    bool has = (uint32_t)lane < m;
+    uint32_t nxt = min(m, 32u);  // next key of q to hand out
+    {
+        uint32_t key[V];
+#pragma unroll
+        for (int w = 0; w < V; w++) key[w] = has ? q[lane * V + w] : 0u;
+        h = fold<V>(T.salt, key);
+#pragma unroll
+        for (int w = 0; w < V; w++) km[w] = key[w] | (w == (int)T.mark_word ? mark_lo : 0u);
+    }
+    while (__any_sync(FULLMASK, has)) {
+        const uint64_t bkt = has ? bucket_of(T, h, r) : 0;
+        sbkt[lane] = has ? bkt : SKIP;
+        if (nprobe) *nprobe += has ? 1u : 0u;
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < CH; it++) {
+            const uint32_t c = it * 32 + lane;
+            const uint32_t k = c / CH, j = c % CH;
+            const unsigned long long b = sbkt[k];
+            if (b != SKIP) cp_async16(stage + k * CH + (j ^ (k & (CH - 1))), T.data + b * (uint64_t)BW + 4 * j);
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        int rc = -1, slot = -1;
+        if (has) {
+            for (int j = 0; j < CH && rc == -1; j++) {
+                const uint4 c4 = stage[lane * CH + (j ^ (lane & (CH - 1)))];
+                const uint32_t w4[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+                for (int t = 0; t < SPC; t++) {
+                    if (rc != -1) break;
+                    bool zero = true, eq = true;
+#pragma unroll
+                    for (int w = 0; w < V; w++) {
+                        zero = zero && w4[t * V + w] == 0u;
+                        eq = eq && w4[t * V + w] == km[w];
+                    }
+                    if (eq) {
+                        rc = FOUND;
+                        slot = j * SPC + t;
+                    } else if (zero) {
+                        rc = -3;  // CAS candidate
+                        slot = j * SPC + t;
+                    }
+                }
+            }
+        }
+        __syncwarp();  // stage and sbkt are free again
+        if (rc == -3) {
+            uint32_t old[V];
+            SlotCas<V>::cas(T.data + bkt * (uint64_t)BW + slot * V, km, old);
+            bool zero = true, eq = true;
+#pragma unroll
+            for (int w = 0; w < V; w++) {
+                zero = zero && old[w] == 0u;
+                eq = eq && old[w] == km[w];
+            }
+            if (zero) {
+                rc = INSERTED;
+            } else if (eq) {
+                rc = FOUND;
+            } else {  // lost the slot to another key: the rest of the bucket
+                int64_t hd;
+                rc = resolve_lane_from<BW, V>(T, bkt, slot + 1, km, &hd);
+            }
+        }
+        bool done = false;
+        if (has) {
+            if (rc == -1 && ++r >= (int)T.k) rc = TABLE_FULL;  // all K buckets full
+            done = rc >= 0;
+        }
+        *full += (done && rc == TABLE_FULL) ? 1u : 0u;
+        // INSERTED keys to the front of q (positions below nxt: consumed)
+        const bool ins = done && rc == INSERTED;
+        const uint32_t im = __ballot_sync(FULLMASK, ins);
+        if (ins) {
+            const uint32_t p = n_ins + __popc(im & lanemask_lt_());
+#pragma unroll
+            for (int w = 0; w < V; w++) q[p * V + w] = km[w] & ~(w == (int)T.mark_word ? mark_lo : 0u);
+        }
+        n_ins += __popc(im);
+        // refill the lanes that finished with the next keys of q
+        const uint32_t dm = __ballot_sync(FULLMASK, done);
+        if (done) {
+            const uint32_t idx = nxt + __popc(dm & lanemask_lt_());
+            has = idx < m;
+            if (has) {
+                uint32_t key[V];
+#pragma unroll
+                for (int w = 0; w < V; w++) key[w] = q[idx * V + w];
+                h = fold<V>(T.salt, key);
+#pragma unroll
+                for (int w = 0; w < V; w++) km[w] = key[w] | (w == (int)T.mark_word ? mark_lo : 0u);
+                r = 0;
+            }
+        }
+        nxt = min(m, nxt + __popc(dm));
+        __syncwarp();
+    }
+    return n_ins;
+}
+
 // FINDORPUT of keys q[0, m) (V words each, shared memory), KB at a time.
 // INSERTED keys are written back, compacted, to the front of q (a key is
 // only ever written at or below the position it was read from); returns
@@ -181,6 +313,9 @@ __device__ __forceinline__ uint32_t probe_staged(const TableDesc& T, uint32_t* q
     using S = Staged<BW, V, KBX>;
     constexpr int KB = S::KB, KPL = S::KPL, CH = S::CH, SPC = S::SPC;
     constexpr unsigned long long SKIP = ~0ull;
+#if GX_REFILL && !GX_TMA
+    if constexpr (KPL == 1) return probe_refill<BW, V>(T, q, m, stage, sbkt, full, nprobe);
+#endif
     const int lane = threadIdx.x & 31;
     uint32_t n_ins = 0;
     for (uint32_t r0 = 0; r0 < m; r0 += KB) {
