@@ -31,6 +31,10 @@
 
 namespace gx {
 
+#ifndef GX_ABSORB_CACHE
+#define GX_ABSORB_CACHE 1  // the block-local dedup cache in front of the inbox probes too
+#endif
+
 template <int BW, int V>
 __global__ void __launch_bounds__(256, GX_STAGED_MINB) k_level_routed(TableDesc T, NetDesc N, LevelArgs A, RouteArgs R,
                                                                       AbsorbArgs AB) {
@@ -64,7 +68,7 @@ __global__ void __launch_bounds__(256, GX_STAGED_MINB) k_absorb(TableDesc T, Lev
     uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
     staged_init(sbkt, S::KB);
     unsigned long long* dcache = reinterpret_cast<unsigned long long*>(smem + L::FIXED);
-    const uint32_t cmask = V <= 2 ? A.cache_mask : 0u;
+    const uint32_t cmask = (V <= 2 && GX_ABSORB_CACHE) ? A.cache_mask : 0u;
     if (cmask) {
         for (uint32_t i = threadIdx.x; i <= cmask; i += blockDim.x) dcache[i] = 0ull;
         __syncthreads();
