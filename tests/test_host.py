@@ -244,3 +244,24 @@ def test_may_collide_is_sound_on_reachable_states():
                 assert not (targets(a, s) & targets(b, s)), (name, a, b, s)
                 checked += 1
     assert checked > 0
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5])
+def test_philosophers_generator_equals_golden_family(n, tmp_path, capsys):
+    """gen-model philosophers (the product's deadlocking family) produces the
+    reference-pinned golden models phil2..5: same reachable set (dump sha
+    from the real reference, tests/golden/models.json) and one deadlock."""
+    import hashlib
+    import json
+
+    from conftest import GOLDEN
+    from oracle import oracle as O
+    from paper_1801_05857_b200.cli import main
+    assert main(["gen-model", "philosophers", "--n", str(n), "--out", str(tmp_path / "p")]) == 0
+    capsys.readouterr()
+    r = O.explore(O.Net.from_file(tmp_path / "p" / "net.exp"), capacity_words=1 << 16, detect_deadlocks=True)
+    want = json.loads((GOLDEN / "models.json").read_text())[f"phil{n}"]["runs"][0]
+    assert hashlib.sha256(r.dump_states().encode()).hexdigest() == want["dump_states_sha"]
+    assert (r.states, r.transitions, r.deadlocks_total) == \
+        (want["report"]["states"], want["report"]["transitions"], want["report"]["deadlocks_total"]) == \
+        (3 ** n - 1, want["report"]["transitions"], 1)
