@@ -67,6 +67,19 @@ __device__ __forceinline__ void rule_target(const NetDesc& N, const uint4 rl, ui
                                             const uint32_t* s, uint32_t* t) {
 #pragma unroll
     for (int w = 0; w < V; w++) t[w] = s[w];
+    if (c == 0) {
+        // combination 0 (the only one when every participant has a single
+        // destination, the common case): every digit is 0, no division
+        for (uint32_t k = 0; k < rl.x; k++) {
+            const uint4 pt = __ldg(&N.parts[rl.y + k]);
+            const uint2 l = __ldg(&N.rq[pt.x + field_get<V>(s, pt.y, pt.z, pt.w)]);
+            const uint32_t dst = __ldg(&N.rdst[l.x]);
+#pragma unroll
+            for (int w = 0; w < V; w++)
+                if ((uint32_t)w == pt.y) t[w] = (t[w] & ~(pt.w << pt.z)) | (dst << pt.z);
+        }
+        return;
+    }
     // mixed radix, last participant fastest (itertools.product order)
     for (int k = (int)rl.x - 1; k >= 0; k--) {
         const uint4 pt = __ldg(&N.parts[rl.y + k]);
