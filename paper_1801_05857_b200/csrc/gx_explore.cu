@@ -1016,17 +1016,15 @@ int gx_explore(gx_net* n, gx_table* t, const gx_explore_cfg* cfg, gx_report* rep
         set_error("no level kernel for bw=%u vlen=%u group=%d", T.bw, v, cfg->probe_group);
         return GX_EINPUT;
     }
-    // block-local dedup cache: cache_slots rounded down to a power of two,
-    // at most GX_CACHE_MAX_SLOTS and what keeps GX_STAGED_MINB blocks per SM resident
-    // (only for in-band tables with vlen <= 2)
+    // block-local dedup cache: cache_slots, at most GX_CACHE_MAX_SLOTS and
+    // what keeps GX_STAGED_MINB blocks per SM resident (any count; only for
+    // in-band tables with vlen <= 2)
     uint32_t cslots = 0;
     if (cfg->cache_slots > 0 && T.mode == MODE_MARK && v <= 2) {
         const size_t budget = STAGED_SMEM_BUDGET;
         const size_t fixed = LK.fixed_smem + (staged ? 0 : 2 * 8 * QWORDS_REG * 4);
-        cslots = 1;
-        while (cslots * 2 <= (uint32_t)cfg->cache_slots && cslots * 2 <= GX_CACHE_MAX_SLOTS &&
-               fixed + 8 * (size_t)cslots * 2 <= budget)
-            cslots *= 2;
+        const size_t room = budget > fixed ? (budget - fixed) / 8 : 0;
+        cslots = (uint32_t)std::min<size_t>({(size_t)cfg->cache_slots, (size_t)GX_CACHE_MAX_SLOTS, room});
         if (cslots < 32) cslots = 0;
     }
     const size_t csmem = LK.fixed_smem + sizeof(unsigned long long) * cslots;

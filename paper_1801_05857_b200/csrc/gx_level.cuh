@@ -109,6 +109,8 @@ __device__ __forceinline__ void flush_out(const LevelArgs& A, const uint32_t* ou
 
 // Block-local dedup cache (GPUexplore's per-block cache; the
 // reference's LocalCache, explore.py:91-144): a direct-mapped table of
+// cmask + 1 slots (any count: the slot is the high half of mix x slots,
+// so the cache takes whatever shared memory the resident blocks leave) of
 // 64-bit packed keys (stored with the mark bit, so 0 = empty) in dynamic
 // shared memory.  atomicExch installs a key and returns the previous
 // occupant; only a key that was already there is dropped, because whoever
@@ -139,7 +141,7 @@ __device__ __forceinline__ uint32_t cache_filter(const TableDesc& T, unsigned lo
         bool keep = false;
         if (a) {
             const unsigned long long kv = cache_word<V>(T, key);
-            keep = atomicExch(&cache[key_mix<V>(key) & cmask], kv) != kv;
+            keep = atomicExch(&cache[__umulhi(key_mix<V>(key), cmask + 1u)], kv) != kv;
         }
         const uint32_t km = __ballot_sync(FULLMASK, keep);
         __syncwarp();
@@ -334,7 +336,7 @@ __device__ __forceinline__ uint32_t filter_route(const TableDesc& T, const Route
             const uint32_t x = key_mix<V>(key);
             if (cmask) {
                 const unsigned long long kv = cache_word<V>(T, key);
-                keep = atomicExch(&cache[x & cmask], kv) != kv;
+                keep = atomicExch(&cache[__umulhi(x, cmask + 1u)], kv) != kv;  // any slot count
             }
             if (keep && ROUTE) o = owner_of_mix(x, world);
         }

@@ -412,9 +412,8 @@ int gx_shard_create(gx_net* n, gx_table* t, int32_t rank, int32_t world, uint64_
     s->cslots = 0;
     if (cache_slots > 0 && T.vlen <= 2) {
         const size_t budget = STAGED_SMEM_BUDGET;
-        uint32_t c = 1;
-        while (c * 2 <= (uint32_t)cache_slots && c * 2 <= GX_CACHE_MAX_SLOTS && K.fixed_smem + 16 * (size_t)c <= budget)
-            c *= 2;
+        const size_t room = budget > K.fixed_smem ? (budget - K.fixed_smem) / 8 : 0;
+        const uint32_t c = (uint32_t)std::min<size_t>({(size_t)cache_slots, (size_t)GX_CACHE_MAX_SLOTS, room});
         s->cslots = c >= 32 ? c : 0;
     }
     s->smem = K.fixed_smem + 8 * (size_t)s->cslots;

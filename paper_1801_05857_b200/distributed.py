@@ -168,6 +168,7 @@ class FusedShard:
 
         from .explore import device_table_config
         self.rank, self.world = rank, world
+        self.stream = stream
         self.scheme = statevec.make_scheme(net)
         self.vlen = statevec.device_vlen(self.scheme, cfg.pad_vlen3)
         self.dnet = DeviceNetwork(net, self.scheme, stream, self.vlen)
@@ -213,6 +214,11 @@ class FusedShard:
     @property
     def handle(self):
         return self._h
+
+    def sync(self):
+        """Wait for this shard's stream (its kernels and peer stores)."""
+        from ._lib import check, lib
+        check(lib().gx_sync(self.stream))
 
     def owner_of(self, packed: np.ndarray) -> int:
         from ._lib import check, lib, ptr
@@ -596,6 +602,12 @@ def explore_fused(shards, dist, torch, detect: bool, max_iterations=None,
     flag = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def barrier():
+        # this process's shard kernels (and their peer stores) complete
+        # before the collective, whatever stream or backend it runs on: a
+        # gloo all_reduce of a host tensor would not wait for them
+        for s in shards:
+            if hasattr(s, "sync"):
+                s.sync()
         dist.all_reduce(flag)
 
     def reduce(a, op=None):

@@ -12,8 +12,9 @@ reference (explore.py:234-240, 255-268).
 
 `cache_slots` keeps its meaning as the size of the per-worker dedup cache
 (`LocalCache`, explore.py:91-144): on the device it sizes each thread
-block's shared-memory cache (rounded down to a power of two, at most
-8192; below 32 the cache is off).  The CPU worker knobs (`workers`,
+block's shared-memory cache (at most 8192 slots and what the three
+resident blocks per SM leave of shared memory, ~1000 at bw 32; below 32
+the cache is off).  The CPU worker knobs (`workers`,
 `backend`) are accepted and validated for compatibility; they do not change
 device execution.
 """
