@@ -411,13 +411,28 @@ __device__ __forceinline__ uint32_t filter_route(const TableDesc& T, const Route
 // cp.async, KB buckets in flight per warp.  All per-warp buffers live in
 // dynamic shared memory: [q 8*QWORDS u32][bucket idx 8*KB u64]
 // [stage 8*STAGE_BYTES][dedup cache].
+#ifndef GX_OVERLAP
+// 1: one-bucket-per-lane tables use level_overlap_body.  Exact (the GPU
+// suite passes with it on) but slower on B200: ring19 1.53 vs 1.92, ring16
+// 2.19 vs 2.81 ·10^9 states/s, peterson6 level 212 vs 152 ms
+// (profiles/round2/s2zp_*; ring16 by slice size 64 / 128 / 256: 227 /
+// 188 / 170 ms vs 142, s2zq_*): a round-sized slice of successors covers the
+// ranges of about a third of the tile's states, so expand_state runs with
+// a third of the lanes active several times per tile, and that issue cost
+// outweighs the load latency it hides (other warps hid most of it already).
+#define GX_OVERLAP 0
+#endif
+
 template <int BW, int V>
 struct StagedSmem {
     using S = Staged<BW, V>;
     static constexpr size_t Q = 8ull * QWORDS * 4;
     static constexpr size_t B = 8ull * S::SB_STRIDE * 8;
     static constexpr size_t ST = 8ull * S::STAGE_BYTES;
-    static constexpr size_t FIXED = Q + B + ST;
+    // per-warp routing scratch (64 u32) of the overlapped body, whose stage
+    // buffer is busy while it routes
+    static constexpr size_t SCR = GX_OVERLAP ? 8ull * 64 * 4 : 0;
+    static constexpr size_t FIXED = Q + B + ST + SCR;
 };
 
 // Inbox keys to FINDORPUT in the same launch as the expansion (the
@@ -429,12 +444,267 @@ struct AbsorbArgs {
     uint64_t cap;
 };
 
+#ifndef GX_OV_CHUNK
+#define GX_OV_CHUNK 128  // successors emitted per probe round
+#endif
+
+// The level body for tables whose warp stages one bucket per lane
+// (probe_refill): the same work as level_staged_body, software-pipelined
+// so that a warp's bucket loads overlap its own expansion.  Each turn of
+// the loop (1) issues the cp.async bucket loads of the lanes' current
+// keys, (2) while they fly, expands the next GX_OV_CHUNK successors of
+// the warp's frontier tile (or loads the next tile) into the pending
+// queue, filtered by the block cache and routed to their owners
+// (filter_route), and (3) resolves the round exactly as probe_refill
+// does -- FOUND / CAS claim / next hash function / TABLE_FULL -- and
+// refills the lanes whose keys are done from the pending queue.  INSERTED
+// keys collect in the queue's last quarter and go to the next frontier a
+// flush at a time.  Each key's probe sequence and CAS protocol are those
+// of hashtable.py:224-280, so the level's results are unchanged; only the
+// interleaving differs.
+template <int BW, int V, bool ROUTE>
+__device__ __forceinline__ void level_overlap_body(const TableDesc& T, const NetDesc& N, const LevelArgs& A,
+                                                   const RouteArgs& R) {
+    using L = StagedSmem<BW, V>;
+    using S = Staged<BW, V>;
+    constexpr int CH = BW / 4, SPC = 4 / V;
+    constexpr uint32_t QCAP = QWORDS / V;
+    constexpr uint32_t OCAP = QCAP / 4;         // inserted keys awaiting a flush
+    constexpr uint32_t PCAP = QCAP - OCAP;      // pending keys
+    constexpr uint32_t CHUNK = GX_OV_CHUNK < PCAP / 2 ? GX_OV_CHUNK : PCAP / 2;
+    constexpr unsigned long long SKIP = ~0ull;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    uint32_t* pq = reinterpret_cast<uint32_t*>(smem) + wid * QWORDS;
+    uint32_t* oq = pq + PCAP * V;
+    unsigned long long* sbkt = reinterpret_cast<unsigned long long*>(smem + L::Q) + wid * S::SB_STRIDE;
+    uint4* stage = reinterpret_cast<uint4*>(smem + L::Q + L::B + (size_t)wid * S::STAGE_BYTES);
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + L::Q + L::B + L::ST) + wid * 64;
+    unsigned long long* dcache = reinterpret_cast<unsigned long long*>(smem + L::FIXED);
+    const uint32_t cmask = V <= 2 ? A.cache_mask : 0u;
+    if (cmask) {
+        for (uint32_t i = threadIdx.x; i <= cmask; i += blockDim.x) dcache[i] = 0ull;
+        __syncthreads();
+    }
+    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    uint64_t base = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * 32;  // next tile
+    unsigned long long trans = 0, expanded = 0, probes = 0, routed = 0;
+    const uint32_t mark_lo = T.mark;
+    // the warp's frontier tile: this lane's state, its successor count n and
+    // exclusive offset, the tile's total and how many are emitted
+    uint32_t s[V];
+    uint32_t n = 0, excl = 0, total = 0, c0 = 0;
+    bool sh = false, tiles = true;
+    // probe lane: key (with the mark), fold, hash function index
+    uint32_t km[V];
+    uint64_t h = 0;
+    int r = 0;
+    bool has = false;
+    uint32_t ph = 0, pt = 0, n_out = 0;  // pending [ph, pt); inserted [0, n_out)
+#pragma unroll
+    for (int w = 0; w < V; w++) s[w] = km[w] = 0u;
+    while (true) {
+        // (1) this round's bucket loads
+        const bool any = __any_sync(FULLMASK, has);
+        const uint64_t bkt = has ? bucket_of(T, h, r) : 0;
+        if (any) {
+            sbkt[lane] = has ? bkt : SKIP;
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < CH; it++) {
+                const uint32_t c = it * 32 + lane;
+                const uint32_t k = c / CH, j = c % CH;
+                const unsigned long long b = sbkt[k];
+                if (b != SKIP) cp_async16(stage + k * CH + (j ^ (k & (CH - 1))), T.data + b * (uint64_t)BW + 4 * j);
+            }
+            cp_async_commit();
+        }
+        // (2) expansion while they fly
+        if (c0 < total) {
+            if (pt + CHUNK > PCAP && ph > 0) {  // slide the pending keys down
+                const uint32_t nw = (pt - ph) * V;
+                for (uint32_t x0 = 0; x0 < nw; x0 += 32) {
+                    const uint32_t x = x0 + lane;
+                    const uint32_t v = x < nw ? pq[ph * V + x] : 0u;
+                    __syncwarp();
+                    if (x < nw) pq[x] = v;
+                    __syncwarp();
+                }
+                pt -= ph;
+                ph = 0;
+            }
+            if (pt + CHUNK <= PCAP) {
+                const uint32_t c1 = min(total, c0 + CHUNK);
+                if (sh && n && excl < c1 && excl + n > c0) {
+                    const uint32_t lo = max(c0, excl) - excl;
+                    const uint32_t hi = min(c1, excl + n) - excl;
+                    uint64_t dummy;
+                    expand_state<V, true>(N, s, &dummy, lo, hi, pq + (uint64_t)(pt + excl + lo - c0) * V);
+                }
+                __syncwarp();
+                uint32_t m = c1 - c0;
+                if (ROUTE || cmask)
+                    m = filter_route<V, ROUTE>(T, R, dcache, cmask, pq + pt * V, m, &A.ctr[LV_OVF], &routed,
+                                               scratch);
+                probes += lane == 0 ? m : 0u;
+                pt += m;
+                c0 = c1;
+            }
+        } else if (tiles) {
+            int stop = 0;
+            if (lane == 0)
+                stop = (*(volatile unsigned long long*)&A.ctr[LV_FULL] != 0ull) ||
+                       (*(volatile unsigned long long*)&A.ctr[LV_OVF] != 0ull);
+            if (__shfl_sync(FULLMASK, stop, 0) || base >= A.nfront) {
+                tiles = false;
+                if (stop) ph = pt;  // abandon the level's remaining keys
+            } else {
+                const uint64_t idx = base + lane;
+                sh = idx < A.nfront;
+                if (sh)
+                    load_state<V>(A.front + idx * V, s);
+                n = 0;
+                if (sh) {
+                    uint64_t cnt = 0;
+                    n = expand_state<V, false>(N, s, &cnt, 0, 0, nullptr);
+                    trans += cnt;
+                    expanded += 1;
+                    if (cnt == 0 && A.detect) {
+                        unsigned long long p = atomicAdd(&A.ctr[LV_DL], 1ull) - A.dl_base;
+                        if (p < A.dl_cap) store_state<V>(A.dl + p * V, s);
+                    }
+                }
+                uint32_t incl = n;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    uint32_t y = __shfl_up_sync(FULLMASK, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                total = __shfl_sync(FULLMASK, incl, 31);
+                excl = incl - n;
+                c0 = 0;
+                base += nwarps * 32;
+            }
+        }
+        // (3) resolve the round
+        if (any) {
+            cp_async_wait0();
+            __syncwarp();
+            int rc = -1, slot = -1;
+            if (has) {
+                for (int j = 0; j < CH && rc == -1; j++) {
+                    const uint4 c4 = stage[lane * CH + (j ^ (lane & (CH - 1)))];
+                    const uint32_t w4[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+                    for (int t = 0; t < SPC; t++) {
+                        if (rc != -1) break;
+                        bool zero = true, eq = true;
+#pragma unroll
+                        for (int w = 0; w < V; w++) {
+                            zero = zero && w4[t * V + w] == 0u;
+                            eq = eq && w4[t * V + w] == km[w];
+                        }
+                        if (eq) {
+                            rc = FOUND;
+                            slot = j * SPC + t;
+                        } else if (zero) {
+                            rc = -3;
+                            slot = j * SPC + t;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (rc == -3) {
+                uint32_t old[V];
+                SlotCas<V>::cas(T.data + bkt * (uint64_t)BW + slot * V, km, old);
+                bool zero = true, eq = true;
+#pragma unroll
+                for (int w = 0; w < V; w++) {
+                    zero = zero && old[w] == 0u;
+                    eq = eq && old[w] == km[w];
+                }
+                if (zero) {
+                    rc = INSERTED;
+                } else if (eq) {
+                    rc = FOUND;
+                } else {
+                    int64_t hd;
+                    rc = resolve_lane_from<BW, V>(T, bkt, slot + 1, km, &hd);
+                }
+            }
+            bool done = false;
+            if (has) {
+                if (rc == -1 && ++r >= (int)T.k) rc = TABLE_FULL;
+                done = rc >= 0;
+            }
+            if (done && rc == TABLE_FULL) atomicExch(&A.ctr[LV_FULL], 1ull);
+            const bool ins = done && rc == INSERTED;
+            const uint32_t im = __ballot_sync(FULLMASK, ins);
+            if (ins) {
+                const uint32_t p = n_out + __popc(im & lanemask_lt());
+#pragma unroll
+                for (int w = 0; w < V; w++) oq[p * V + w] = km[w] & ~(w == (int)T.mark_word ? mark_lo : 0u);
+            }
+            n_out += __popc(im);
+            has = has && !done;
+            if (n_out + 32 > OCAP) {
+                __syncwarp();
+                flush_out<V>(A, oq, n_out);
+                n_out = 0;
+                __syncwarp();
+            }
+        }
+        // refill the idle lanes from the pending keys
+        const bool idle = !has;
+        const uint32_t dm = __ballot_sync(FULLMASK, idle);
+        if (idle) {
+            const uint32_t idx = ph + __popc(dm & lanemask_lt());
+            if (idx < pt) {
+                uint32_t key[V];
+#pragma unroll
+                for (int w = 0; w < V; w++) key[w] = pq[idx * V + w];
+                h = fold<V>(T.salt, key);
+#pragma unroll
+                for (int w = 0; w < V; w++) km[w] = key[w] | (w == (int)T.mark_word ? mark_lo : 0u);
+                r = 0;
+                has = true;
+            }
+        }
+        ph = min(pt, ph + __popc(dm));
+        __syncwarp();
+        if (!tiles && c0 >= total && ph >= pt && !__any_sync(FULLMASK, has)) break;
+    }
+    if (n_out) flush_out<V>(A, oq, n_out);
+    trans = warp_sum(trans);
+    expanded = warp_sum(expanded);
+    probes = warp_sum(probes);
+    if (ROUTE) {
+        __threadfence_system();  // peer inbox stores visible before the level barrier
+    }
+    if (lane == 0) {
+        if (ROUTE && routed) atomicAdd(&A.ctr[LV_ROUTED], routed);
+        if (trans) atomicAdd(&A.ctr[LV_TRANS], trans);
+        if (expanded) atomicAdd(&A.ctr[LV_EXP], expanded);
+        if (probes) atomicAdd(&A.ctr[LV_PROBES], probes);
+    }
+}
+
 template <int BW, int V, bool ROUTE>
 __device__ __forceinline__ void level_staged_body(const TableDesc& T, const NetDesc& N, const LevelArgs& A,
                                                   const RouteArgs& R, const AbsorbArgs AB = AbsorbArgs{nullptr, nullptr, 0}) {
     using L = StagedSmem<BW, V>;
     using S = Staged<BW, V>;
     constexpr int QCAP = QWORDS / V;
+#if GX_OVERLAP && GX_REFILL && !GX_TMA
+    if constexpr (S::KPL == 1) {
+        if (!(V <= 2 && A.gfilter_mask) && !(ROUTE && AB.keys)) {
+            level_overlap_body<BW, V, ROUTE>(T, N, A, R);
+            return;
+        }
+    }
+#endif
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
