@@ -174,6 +174,23 @@ __device__ __forceinline__ void tma_wait(unsigned long long* mbar, uint32_t pari
 #ifndef GX_REFILL
 #define GX_REFILL 1  // one key per lane, lanes refilled as their keys resolve (see probe_refill)
 #endif
+#ifndef GX_PREFETCH
+// 1: probe_refill prefetches the next round's first buckets into L2 while
+// a round's loads fly.  Exact, but slower on B200: ring19 1.63 vs 1.92,
+// ring16 2.57 vs 3.07 ·10^9 states/s (peterson6 level 150 vs 152 ms),
+// profiles/round2/s2zr_*: the extra fold + bucket per key and round and the
+// second request per probe cost more than the latency they hide.
+#define GX_PREFETCH 0
+#endif
+
+// a 128-byte line into L2: a 16-byte cp.async with the 128 B L2 prefetch
+// size into a dump slot (a per-lane instruction; the bulk L2 prefetch
+// takes a uniform address and compiles to a 32-pass loop per warp)
+__device__ __forceinline__ void prefetch_l2_128(void* dump, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(dump);
+    asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // FINDORPUT of keys q[0, m) with every lane owning one key at a time and a
 // round = one bucket per lane: all 32 buckets of a round are staged with
@@ -222,7 +239,27 @@ __device__ __forceinline__ uint32_t probe_refill(const TableDesc& T, uint32_t* q
             const unsigned long long b = sbkt[k];
             if (b != SKIP) cp_async16(stage + k * CH + (j ^ (k & (CH - 1))), T.data + b * (uint64_t)BW + 4 * j);
         }
+#if GX_PREFETCH
+        // while the round's loads fly: the first buckets of the next 32
+        // queued keys (the keys lanes take when theirs resolve) into L2, so
+        // the round that stages them finds them there; their folds travel
+        // to the taking lanes by shuffle.  The prefetches are their own
+        // cp.async group, which the round does not wait for.
+        __shared__ uint4 pf_dump[32];  // never read
+        cp_async_commit();
+        uint64_t hn = 0;
+        if (nxt + lane < m) {
+            uint32_t key[V];
+#pragma unroll
+            for (int w = 0; w < V; w++) key[w] = q[(nxt + lane) * V + w];
+            hn = fold<V>(T.salt, key);
+            prefetch_l2_128(pf_dump + lane, T.data + bucket_of(T, hn, 0) * (uint64_t)BW);
+        }
+        cp_async_commit();
+        cp_async_wait1();
+#else
         cp_async_wait_all();
+#endif
         __syncwarp();
         int rc = -1, slot = -1;
         if (has) {
@@ -284,6 +321,9 @@ __device__ __forceinline__ uint32_t probe_refill(const TableDesc& T, uint32_t* q
         n_ins += __popc(im);
         // refill the lanes that finished with the next keys of q
         const uint32_t dm = __ballot_sync(FULLMASK, done);
+#if GX_PREFETCH
+        const uint64_t hs = __shfl_sync(FULLMASK, hn, (int)(__popc(dm & lanemask_lt_()) & 31));
+#endif
         if (done) {
             const uint32_t idx = nxt + __popc(dm & lanemask_lt_());
             has = idx < m;
@@ -291,7 +331,11 @@ __device__ __forceinline__ uint32_t probe_refill(const TableDesc& T, uint32_t* q
                 uint32_t key[V];
 #pragma unroll
                 for (int w = 0; w < V; w++) key[w] = q[idx * V + w];
+#if GX_PREFETCH
+                h = hs;
+#else
                 h = fold<V>(T.salt, key);
+#endif
 #pragma unroll
                 for (int w = 0; w < V; w++) km[w] = key[w] | (w == (int)T.mark_word ? mark_lo : 0u);
                 r = 0;
@@ -300,6 +344,9 @@ __device__ __forceinline__ uint32_t probe_refill(const TableDesc& T, uint32_t* q
         nxt = min(m, nxt + __popc(dm));
         __syncwarp();
     }
+#if GX_PREFETCH
+    cp_async_wait0();  // the last prefetch group
+#endif
     return n_ins;
 }
 
