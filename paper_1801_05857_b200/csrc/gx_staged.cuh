@@ -174,6 +174,15 @@ __device__ __forceinline__ void tma_wait(unsigned long long* mbar, uint32_t pari
 #ifndef GX_REFILL
 #define GX_REFILL 1  // one key per lane, lanes refilled as their keys resolve (see probe_refill)
 #endif
+#ifndef GX_DEFER_CAS
+// 1: probe_refill judges a claim CAS one round after issuing it (the warp
+// does not wait for the atomic; the lane sits out one round).  Exact (the
+// GPU suite passes with it on), but slower on B200: ring19 1.85 vs 1.92,
+// ring16 2.93 vs 3.07 ·10^9 states/s, peterson6 level 156 vs 152 ms
+// (profiles/round2/s2zu_*): a lane idle for a whole round costs more than
+// the CAS round trip the warp would otherwise wait for.
+#define GX_DEFER_CAS 0
+#endif
 #ifndef GX_PREFETCH
 // 1: probe_refill prefetches the next round's first buckets into L2 while
 // a round's loads fly.  Exact, but slower on B200: ring19 1.63 vs 1.92,
@@ -227,10 +236,22 @@ __device__ __forceinline__ uint32_t probe_refill(const TableDesc& T, uint32_t* q
 #pragma unroll
         for (int w = 0; w < V; w++) km[w] = key[w] | (w == (int)T.mark_word ? mark_lo : 0u);
     }
+#if GX_DEFER_CAS
+    bool pend = false;  // this lane's claim CAS is in flight (issued last round)
+    uint32_t pold[V];
+    int pslot = 0;
+#pragma unroll
+    for (int w = 0; w < V; w++) pold[w] = 0u;
+#endif
     while (__any_sync(FULLMASK, has)) {
+#if GX_DEFER_CAS
+        const bool ld = has && !pend;  // lanes that stage a bucket this round
+#else
+        const bool ld = has;
+#endif
         const uint64_t bkt = has ? bucket_of(T, h, r) : 0;
-        sbkt[lane] = has ? bkt : SKIP;
-        if (nprobe) *nprobe += has ? 1u : 0u;
+        sbkt[lane] = ld ? bkt : SKIP;
+        if (nprobe) *nprobe += ld ? 1u : 0u;
         __syncwarp();
 #pragma unroll
         for (int it = 0; it < CH; it++) {
@@ -262,7 +283,7 @@ __device__ __forceinline__ uint32_t probe_refill(const TableDesc& T, uint32_t* q
 #endif
         __syncwarp();
         int rc = -1, slot = -1;
-        if (has) {
+        if (ld) {
             for (int j = 0; j < CH && rc == -1; j++) {
                 const uint4 c4 = stage[lane * CH + (j ^ (lane & (CH - 1)))];
                 const uint32_t w4[4] = {c4.x, c4.y, c4.z, c4.w};
@@ -286,6 +307,34 @@ __device__ __forceinline__ uint32_t probe_refill(const TableDesc& T, uint32_t* q
             }
         }
         __syncwarp();  // stage and sbkt are free again
+#if GX_DEFER_CAS
+        // the claim CAS is judged one round after it was issued: the warp
+        // does not wait for the atomic's round trip, the lane just sits out
+        // one round's load.  Same judgement as below.
+        if (pend) {
+            bool zero = true, eq = true;
+#pragma unroll
+            for (int w = 0; w < V; w++) {
+                zero = zero && pold[w] == 0u;
+                eq = eq && pold[w] == km[w];
+            }
+            if (zero) {
+                rc = INSERTED;
+            } else if (eq) {
+                rc = FOUND;
+            } else {  // lost the slot to another key: the rest of the bucket
+                int64_t hd;
+                rc = resolve_lane_from<BW, V>(T, bkt, pslot + 1, km, &hd);
+            }
+            pend = false;
+        }
+        if (rc == -3) {
+            SlotCas<V>::cas(T.data + bkt * (uint64_t)BW + slot * V, km, pold);
+            pslot = slot;
+            pend = true;
+            rc = -2;  // in flight: neither done nor a full bucket
+        }
+#else
         if (rc == -3) {
             uint32_t old[V];
             SlotCas<V>::cas(T.data + bkt * (uint64_t)BW + slot * V, km, old);
@@ -304,6 +353,7 @@ __device__ __forceinline__ uint32_t probe_refill(const TableDesc& T, uint32_t* q
                 rc = resolve_lane_from<BW, V>(T, bkt, slot + 1, km, &hd);
             }
         }
+#endif
         bool done = false;
         if (has) {
             if (rc == -1 && ++r >= (int)T.k) rc = TABLE_FULL;  // all K buckets full
